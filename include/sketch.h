@@ -1,0 +1,143 @@
+/*
+ * sketch.h -- C ABI of libsketch.so, the B200 (sm_100a) hot path of arXiv 2603.20966
+ * "Communication Lower Bounds and Algorithms for Sketching with Random Dense Matrices".
+ *
+ * Operations (PAPER.md line numbers, LaTeX source):
+ *   sketch_apply   B = A * Omega,        A in R^{n1 x n2}, Omega in R^{n2 x r}   (sec. 1)
+ *   nystrom_core   B = A * Omega, C = Omega^T * B  (= Omega^T A Omega)          (sec. 1)
+ *   *_block        the local products of Alg. 1 line "B-bar_ik = A_ij * Omega_jk" and
+ *                  Alg. 2 lines "B-hat-bar = A_ij Omega_jk" / "C-bar = Omega^T_i'j' B_i'k'"
+ *                  (PAPER.md:594), with global offsets selecting the rows of Omega.
+ * Omega is never stored in HBM nor communicated: every kernel regenerates the tiles it needs from
+ * a counter-based Philox4x32-10 stream with a shared seed (sec. 6.3), inside
+ * the GEMM, straight into swizzled shared memory.  Entry (j,k) of Omega is a pure function of
+ * (seed, dist, global row j, global column k) -- reading O1 in DESIGN.md:
+ *   GAUSSIAN   Box-Muller on words of Philox((j>>2), k, tag 0): rows 4q,4q+1 use (x0,x1), rows
+ *              4q+2,4q+3 use (x2,x3); u1 = ((w1>>8)+1)/2^24, u2 = (w2>>8)/2^24,
+ *              z = sqrt(-2 ln u1) * (cos 2 pi u2 for even j | sin 2 pi u2 for odd j).  Unscaled N(0,1).
+ *   RADEMACHER bit (j&31) of word ((j>>5)&3) of Philox((j>>7), k, tag 1); set bit -> -1, else +1.
+ *   UNIFORM    (x[j&3] >> 8) / 2^24 in [0,1) from the tag-0 call (the paper's experiment).
+ *
+ * Conventions (all entry points):
+ *   - matrices are fp32, ROW-MAJOR, leading dimensions in ELEMENTS;
+ *   - every matrix / workspace pointer is a DEVICE pointer (cudaMalloc / torch CUDA memory) unless
+ *     stated otherwise; `stream` is a cudaStream_t (NULL = legacy default stream);
+ *   - the caller owns A, B, C, the workspace and the stream; the library owns only the handle
+ *     (no device allocations); A is read-only; B and C are overwritten (no beta-accumulate);
+ *     outputs must not alias inputs;
+ *   - all validation is synchronous and happens before any launch: an error return means nothing
+ *     was enqueued.  Asynchronous device faults surface as SK_ERR_CUDA from a later call;
+ *   - no exception crosses the ABI; sketch_last_error() gives a thread-local detail string;
+ *   - handles are immutable after configuration (sketch_set_*) and may be used concurrently from
+ *     several host threads on different streams.
+ *   - results are deterministic: fixed-order split-K and core reductions, so identical calls give
+ *     bit-identical outputs.
+ */
+#ifndef PAPER_2603_20966_B200_SKETCH_H
+#define PAPER_2603_20966_B200_SKETCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sk_sketch_s* sk_sketch_t; /* opaque, library-owned */
+
+typedef enum {
+    SK_DIST_GAUSSIAN = 0,   /* default: N(0,1) entries                      */
+    SK_DIST_RADEMACHER = 1, /* +-1 entries (north-star extension, c3 workload)              */
+    SK_DIST_UNIFORM = 2     /* U[0,1) entries (the Philox-uniform Omega of PAPER.md:1190)   */
+} sk_dist_t;
+
+typedef enum {
+    SK_MODE_TF32X3 = 0, /* default, fp32-accurate: A_hi*O_hi + A_hi*O_lo + A_lo*O_hi on tf32 MMAs */
+    SK_MODE_TF32 = 1,   /* one tf32 MMA per product (A read as tf32, Omega rounded RN to tf32)   */
+    SK_MODE_BF16 = 2    /* A and Omega rounded RN to bf16 on chip, fp32 accumulation             */
+} sk_mode_t;
+
+typedef enum {
+    SK_OMEGA_ACCURATE = 0, /* <= 2 ulp Box-Muller (logf/sqrtf/sincospif); required for TF32X3   */
+    SK_OMEGA_FAST = 1      /* MUFU lg2/sqrt/sin/cos Box-Muller; tf32/bf16 modes only (reading R5) */
+} sk_omega_transform_t;
+
+typedef enum {
+    SK_SUCCESS = 0,
+    SK_ERR_INVALID_VALUE = 1,  /* bad scalar argument, NULL pointer, out-of-extent block        */
+    SK_ERR_SHAPE_MISMATCH = 2, /* n2 != handle n2, ld < row length, ...                          */
+    SK_ERR_ALIGNMENT = 3,      /* A not 16-byte aligned or lda % 4 != 0 (TMA requirement)        */
+    SK_ERR_UNSUPPORTED = 4,    /* valid request outside what this build implements              */
+    SK_ERR_WORKSPACE = 5,      /* ws_bytes smaller than sketch_*_workspace_size reported         */
+    SK_ERR_CUDA = 6,           /* CUDA runtime / driver error (launch or earlier async fault)    */
+    SK_ERR_NCCL = 7            /* reserved for the native collective layer                       */
+} sk_status_t;
+
+/* Create a handle for Omega in R^{n2 x r} drawn from `dist` with 64-bit `seed`.
+ * n2 is the global number of rows of Omega (= columns of the full A); r >= 1, r <= 4096.
+ * Errors: SK_ERR_INVALID_VALUE (out == NULL, n2 < 1, r < 1, r > 4096, unknown dist). */
+sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, sk_sketch_t* out);
+sk_status_t sketch_destroy(sk_sketch_t h);
+
+/* Precision mode (default SK_MODE_TF32X3).  Errors: SK_ERR_INVALID_VALUE. */
+sk_status_t sketch_set_mode(sk_sketch_t h, sk_mode_t mode);
+/* Gaussian transform used INSIDE the GEMMs (sketch_generate always uses the accurate one).
+ * SK_OMEGA_FAST with SK_MODE_TF32X3 is rejected at apply time with SK_ERR_UNSUPPORTED. */
+sk_status_t sketch_set_omega_transform(sk_sketch_t h, sk_omega_transform_t t);
+/* Tuning override for the split-K factor of the sketch GEMM (0 = automatic, else 1..64). */
+sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k);
+
+/* Bytes of device workspace needed by sketch_apply / sketch_apply_block on n1 rows and
+ * nystrom_core / core_apply_block (split-K partials of B and per-CTA r x r partials of C).
+ * One size covers every entry point for that n1 (n for nystrom_core). */
+sk_status_t sketch_workspace_size(sk_sketch_t h, int64_t n1, size_t* bytes);
+
+/* B[n1 x r] = A[n1 x n2] * Omega[0:n2, 0:r].  n2 must equal the handle's n2.
+ * A: device, lda >= n2, lda % 4 == 0, 16-byte aligned.  B: device, ldb >= r.
+ * ws: device workspace of ws_bytes >= sketch_workspace_size(h, n1). */
+sk_status_t sketch_apply(sk_sketch_t h, const float* A, int64_t n1, int64_t n2, int64_t lda,
+                         float* B, int64_t ldb, void* ws, size_t ws_bytes, void* stream);
+
+/* Nystrom core: B[n x r] = A Omega and C[r x r] = Omega^T B for square A
+ * (n must equal the handle's n2; symmetry of A is assumed by the method, not checked).
+ * C is the raw product Omega^T B (not symmetrised, reading R10). */
+sk_status_t nystrom_core(sk_sketch_t h, const float* A, int64_t n, int64_t lda, float* B,
+                         int64_t ldb, float* C, int64_t ldc, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* Block forms for the distributed layouts (Alg. 1 / Alg. 2 with p3 = q3 = 1):
+ *   sketch_apply_block: B_part[m x r] = A_blk[m x k] * Omega[k0 : k0+k, 0:r]
+ *     (column 0 of A_blk pairs with global Omega row k0; requires k0 + k <= handle n2).
+ *   core_apply_block:   C_part[r x r] = Omega[i0 : i0+m, 0:r]^T * B_blk[m x r]
+ *     (row 0 of B_blk pairs with global Omega row i0; requires i0 + m <= handle n2). */
+sk_status_t sketch_apply_block(sk_sketch_t h, const float* A_blk, int64_t m, int64_t k,
+                               int64_t lda, int64_t k0, float* B_part, int64_t ldb, void* ws,
+                               size_t ws_bytes, void* stream);
+sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb,
+                             int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
+                             void* stream);
+
+/* Test / debug: materialise Omega[row0 : row0+nrows, col0 : col0+ncols] (fp32, accurate transform)
+ * or the raw Philox word each entry derives from (x[j&3] for tag 0, x[(j>>5)&3] for tag 1),
+ * row-major into device memory `out` with leading dimension ld >= ncols.
+ * Errors: SK_ERR_INVALID_VALUE if the block leaves [0, 2^62) x [0, r) or out == NULL. */
+sk_status_t sketch_generate(sk_sketch_t h, int64_t row0, int64_t nrows, int64_t col0,
+                            int64_t ncols, float* out, int64_t ld, void* stream);
+sk_status_t sketch_generate_bits(sk_sketch_t h, int64_t row0, int64_t nrows, int64_t col0,
+                                 int64_t ncols, uint32_t* out, int64_t ld, void* stream);
+
+/* Test / debug: evaluate the device Box-Muller transform on caller-given word pairs
+ * (w1[i], w2[i]) -> out_even[i] = R cos, out_odd[i] = R sin; `transform` selects the variant.
+ * All pointers device, n >= 0. */
+sk_status_t sketch_debug_box_muller(const uint32_t* w1, const uint32_t* w2, int64_t n,
+                                    sk_omega_transform_t transform, float* out_even,
+                                    float* out_odd, void* stream);
+
+const char* sketch_status_string(sk_status_t st);
+const char* sketch_last_error(void); /* thread-local detail of the last failing call */
+const char* sketch_build_info(void); /* arch / version string baked in at compile time */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PAPER_2603_20966_B200_SKETCH_H */

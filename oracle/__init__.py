@@ -69,6 +69,7 @@ def _load():
             lib.oracle_omega_words.argtypes = [u64, i32, i64, i64, i64, i64, u32p, i64]
             lib.oracle_sketch.argtypes = [u64, i32, f32p, i64, i64, i64, i64, i64, f64p, i64]
             lib.oracle_core.argtypes = [u64, i32, f64p, i64, i64, i64, i64, f64p, i64]
+            lib.oracle_box_muller_many.argtypes = [u32p, u32p, i64, f32p, f32p]
             lib.oracle_num_threads.restype = i32
             lib.oracle_set_num_threads.argtypes = [i32]
             _lib = lib
@@ -98,6 +99,20 @@ def box_muller(w1: int, w2: int) -> tuple:
     ze, zo = ctypes.c_double(), ctypes.c_double()
     lib.oracle_box_muller(ctypes.c_uint32(w1), ctypes.c_uint32(w2), ctypes.byref(ze), ctypes.byref(zo))
     return ze.value, zo.value
+
+
+def box_muller_many(w1: np.ndarray, w2: np.ndarray) -> tuple:
+    """Correctly rounded fp32 (z_even, z_odd) for arrays of word pairs."""
+    lib = _load()
+    w1 = np.ascontiguousarray(w1, dtype=np.uint32)
+    w2 = np.ascontiguousarray(w2, dtype=np.uint32)
+    n = w1.size
+    ze = np.empty(n, dtype=np.float32)
+    zo = np.empty(n, dtype=np.float32)
+    if n:
+        lib.oracle_box_muller_many(_ptr(w1, ctypes.c_uint32), _ptr(w2, ctypes.c_uint32), n,
+                                   _ptr(ze, ctypes.c_float), _ptr(zo, ctypes.c_float))
+    return ze, zo
 
 
 def omega(seed: int, dist, row0: int, nrows: int, col0: int, ncols: int) -> np.ndarray:

@@ -223,3 +223,17 @@ void oracle_set_num_threads(int n)
     (void)n;
 #endif
 }
+
+/* Vectorised oracle_box_muller for exhaustive transform checks: fp64 results rounded once
+ * to fp32 (RN), i.e. the correctly rounded reference Gaussians. */
+void oracle_box_muller_many(const uint32_t *w1, const uint32_t *w2, int64_t n,
+                            float *z_even, float *z_odd)
+{
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double ze, zo;
+        oracle_box_muller(w1[i], w2[i], &ze, &zo);
+        z_even[i] = (float)ze;
+        z_odd[i] = (float)zo;
+    }
+}

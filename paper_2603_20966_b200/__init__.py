@@ -1,0 +1,264 @@
+"""paper_2603_20966_b200 -- B200-native sketch B = A*Omega and Nystrom core C = Omega^T*B.
+
+Thin ctypes binding over ``libsketch.so`` (C ABI in ``include/sketch.h``).  This module only
+marshals arguments: torch tensors -> device pointers, torch's current stream -> cudaStream_t,
+workspace allocation.  Every step of the hot path runs in the library's CUDA kernels; there is
+no CPU fallback -- without the extension or a GPU every compute call raises.
+
+PAPER.md references: problem statement PAPER.md:106-122 (sec. 1); Omega regenerated from a
+shared-seed counter-based Philox stream, PAPER.md:1185-1190 (sec. 6.3).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+__all__ = ["Sketch", "SketchError", "load_library", "library_path", "EXPORTED_SYMBOLS",
+           "GAUSSIAN", "RADEMACHER", "UNIFORM", "MODES"]
+
+GAUSSIAN, RADEMACHER, UNIFORM = 0, 1, 2
+_DISTS = {"gaussian": GAUSSIAN, "rademacher": RADEMACHER, "uniform": UNIFORM}
+MODES = {"tf32x3": 0, "tf32": 1, "bf16": 2}
+_OMEGA = {"accurate": 0, "fast": 1}
+
+EXPORTED_SYMBOLS = (
+    "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
+    "sketch_set_split_k", "sketch_workspace_size", "sketch_apply", "nystrom_core",
+    "sketch_apply_block", "core_apply_block", "sketch_generate", "sketch_generate_bits",
+    "sketch_debug_box_muller", "sketch_status_string", "sketch_last_error", "sketch_build_info",
+)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+_lock = threading.Lock()
+
+
+class SketchError(RuntimeError):
+    def __init__(self, status: int, name: str, detail: str):
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+        self.name = name
+
+
+def library_path() -> str:
+    return os.path.join(_HERE, "libsketch.so")
+
+
+def load_library(build_if_missing: bool = True):
+    """Load libsketch.so (building it in-tree with nvcc if absent or stale)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        from . import build as _build
+        if build_if_missing:
+            _build.build()
+        path = library_path()
+        if not os.path.exists(path):
+            raise SketchError(-1, "SK_ERR_NOT_BUILT", f"{path} missing (run __graft_entry__.build())")
+        lib = ctypes.CDLL(path)
+        i64, u64, i32, vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p
+        sz = ctypes.c_size_t
+        lib.sketch_create.argtypes = [u64, ctypes.c_int, i64, i64, ctypes.POINTER(vp)]
+        lib.sketch_destroy.argtypes = [vp]
+        lib.sketch_set_mode.argtypes = [vp, ctypes.c_int]
+        lib.sketch_set_omega_transform.argtypes = [vp, ctypes.c_int]
+        lib.sketch_set_split_k.argtypes = [vp, i32]
+        lib.sketch_workspace_size.argtypes = [vp, i64, ctypes.POINTER(sz)]
+        lib.sketch_apply.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, sz, vp]
+        lib.nystrom_core.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
+        lib.sketch_apply_block.argtypes = [vp, vp, i64, i64, i64, i64, vp, i64, vp, sz, vp]
+        lib.core_apply_block.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, sz, vp]
+        lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
+        lib.sketch_generate_bits.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
+        lib.sketch_debug_box_muller.argtypes = [vp, vp, i64, ctypes.c_int, vp, vp, vp]
+        lib.sketch_status_string.argtypes = [ctypes.c_int]
+        lib.sketch_status_string.restype = ctypes.c_char_p
+        lib.sketch_last_error.restype = ctypes.c_char_p
+        lib.sketch_build_info.restype = ctypes.c_char_p
+        for name in EXPORTED_SYMBOLS:
+            if name not in ("sketch_status_string", "sketch_last_error", "sketch_build_info"):
+                getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        lib = load_library()
+        raise SketchError(status, lib.sketch_status_string(status).decode(),
+                          lib.sketch_last_error().decode())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _require_cuda(*tensors):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise SketchError(-1, "SK_ERR_NO_GPU", "no CUDA device: the sketch runs only on the GPU")
+    for t in tensors:
+        if t is not None and (not t.is_cuda or t.dtype != torch.float32):
+            raise SketchError(1, "SK_ERR_INVALID_VALUE", "expected float32 CUDA tensors")
+        if t is not None and t.dim() == 2 and t.stride(1) != 1:
+            raise SketchError(1, "SK_ERR_INVALID_VALUE", "expected row-major tensors (stride(1) == 1)")
+
+
+def _tma_ready(A):
+    """A with a 16-byte-aligned base and row stride (TMA's requirement, SK_ERR_ALIGNMENT in the ABI).
+
+    Contiguous inputs whose row length is not a multiple of 4 fp32 are copied once into a padded
+    buffer (argument marshalling; pass an aligned A to avoid the extra pass over HBM)."""
+    if A.dim() == 2 and A.shape[0] > 0 and (A.stride(0) % 4 != 0 or A.data_ptr() % 16 != 0):
+        torch = _torch()
+        n1, n2 = A.shape
+        buf = torch.empty((n1, (n2 + 3) // 4 * 4), dtype=A.dtype, device=A.device)[:, :n2]
+        buf.copy_(A)
+        return buf
+    return A
+
+
+class Sketch:
+    """Omega in R^{n2 x r} drawn from ``dist`` with ``seed``; never materialised on the hot path.
+
+    mode: 'tf32x3' (fp32-accurate), 'tf32', 'bf16'; omega: 'accurate' | 'fast' Box-Muller.
+    """
+
+    def __init__(self, seed: int, dist, n2: int, r: int, mode: str = "tf32",
+                 omega: str = "accurate", split_k: int = 0):
+        self._lib = load_library()
+        self.seed, self.n2, self.r = int(seed), int(n2), int(r)
+        self.dist = _DISTS[dist] if isinstance(dist, str) else int(dist)
+        self.mode, self.omega = mode, omega
+        h = ctypes.c_void_p()
+        _check(self._lib.sketch_create(self.seed, self.dist, self.n2, self.r, ctypes.byref(h)))
+        self._h = h
+        _check(self._lib.sketch_set_mode(h, MODES[mode]))
+        _check(self._lib.sketch_set_omega_transform(h, _OMEGA[omega]))
+        _check(self._lib.sketch_set_split_k(h, int(split_k)))
+        self._ws = {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.sketch_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------------ workspace
+    def workspace_size(self, n1: int) -> int:
+        n = ctypes.c_size_t()
+        _check(self._lib.sketch_workspace_size(self._h, int(n1), ctypes.byref(n)))
+        return int(n.value)
+
+    def workspace(self, n1: int, device=None):
+        torch = _torch()
+        nbytes = self.workspace_size(n1)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        key = (dev.index, nbytes)
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = torch.empty(max(nbytes, 16) // 4 + 4, dtype=torch.float32, device=dev)
+            self._ws = {key: ws}
+        return ws
+
+    # ------------------------------------------------------------------ hot path
+    def apply(self, A, out=None, stream=None):
+        """B = A Omega for A (n1 x n2) fp32 CUDA, row-major."""
+        torch = _torch()
+        _require_cuda(A, out)
+        n1, n2 = A.shape
+        A = _tma_ready(A)
+        if out is None:
+            out = torch.empty((n1, self.r), dtype=torch.float32, device=A.device)
+        ws = self.workspace(n1, A.device)
+        _check(self._lib.sketch_apply(self._h, A.data_ptr(), n1, n2, A.stride(0), out.data_ptr(),
+                                      out.stride(0), ws.data_ptr(), ws.numel() * 4, _stream_ptr(stream)))
+        return out
+
+    def apply_block(self, A_blk, k0: int, out=None, stream=None):
+        """B_part = A_blk Omega[k0:k0+k] (block form of Alg. 1)."""
+        torch = _torch()
+        _require_cuda(A_blk, out)
+        m, k = A_blk.shape
+        A_blk = _tma_ready(A_blk)
+        if out is None:
+            out = torch.empty((m, self.r), dtype=torch.float32, device=A_blk.device)
+        ws = self.workspace(m, A_blk.device)
+        _check(self._lib.sketch_apply_block(self._h, A_blk.data_ptr(), m, k, A_blk.stride(0), int(k0),
+                                            out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
+                                            _stream_ptr(stream)))
+        return out
+
+    def core_block(self, B_blk, i0: int, out=None, stream=None):
+        """C_part = Omega[i0:i0+m]^T B_blk (Alg. 2 second product)."""
+        torch = _torch()
+        _require_cuda(B_blk, out)
+        m = B_blk.shape[0]
+        if out is None:
+            out = torch.empty((self.r, self.r), dtype=torch.float32, device=B_blk.device)
+        ws = self.workspace(m, B_blk.device)
+        _check(self._lib.core_apply_block(self._h, B_blk.data_ptr(), m, B_blk.stride(0), int(i0),
+                                          out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
+                                          _stream_ptr(stream)))
+        return out
+
+    def nystrom_core(self, A, B=None, C=None, stream=None):
+        """(B, C) = (A Omega, Omega^T A Omega) for square A."""
+        torch = _torch()
+        _require_cuda(A, B, C)
+        n = A.shape[0]
+        A = _tma_ready(A)
+        if B is None:
+            B = torch.empty((n, self.r), dtype=torch.float32, device=A.device)
+        if C is None:
+            C = torch.empty((self.r, self.r), dtype=torch.float32, device=A.device)
+        ws = self.workspace(n, A.device)
+        _check(self._lib.nystrom_core(self._h, A.data_ptr(), n, A.stride(0), B.data_ptr(), B.stride(0),
+                                      C.data_ptr(), C.stride(0), ws.data_ptr(), ws.numel() * 4,
+                                      _stream_ptr(stream)))
+        return B, C
+
+    # ------------------------------------------------------------------ test / debug
+    def generate(self, row0: int, nrows: int, col0: int = 0, ncols=None, stream=None):
+        torch = _torch()
+        _require_cuda()
+        ncols = self.r - col0 if ncols is None else ncols
+        out = torch.empty((nrows, ncols), dtype=torch.float32, device="cuda")
+        _check(self._lib.sketch_generate(self._h, row0, nrows, col0, ncols, out.data_ptr(),
+                                         max(ncols, 1), _stream_ptr(stream)))
+        return out
+
+    def generate_bits(self, row0: int, nrows: int, col0: int = 0, ncols=None, stream=None):
+        torch = _torch()
+        _require_cuda()
+        ncols = self.r - col0 if ncols is None else ncols
+        out = torch.empty((nrows, ncols), dtype=torch.int32, device="cuda")
+        _check(self._lib.sketch_generate_bits(self._h, row0, nrows, col0, ncols, out.data_ptr(),
+                                              max(ncols, 1), _stream_ptr(stream)))
+        return out
+
+
+def debug_box_muller(w1, w2, transform: str = "accurate", stream=None):
+    """Device Box-Muller on word pairs (int32 CUDA tensors holding uint32 bits)."""
+    torch = _torch()
+    lib = load_library()
+    _require_cuda()
+    n = w1.numel()
+    oe = torch.empty(n, dtype=torch.float32, device=w1.device)
+    oo = torch.empty(n, dtype=torch.float32, device=w1.device)
+    _check(lib.sketch_debug_box_muller(w1.data_ptr(), w2.data_ptr(), n, _OMEGA[transform],
+                                       oe.data_ptr(), oo.data_ptr(), _stream_ptr(stream)))
+    return oe, oo

@@ -1,0 +1,434 @@
+// api.cu -- the C ABI declared in include/sketch.h: handle, validation, launch planning,
+// TMA tensor-map encoding, and the call sequences of sketch_apply / nystrom_core.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/sketch.h"
+#include "kernels.cuh"
+
+struct sk_sketch_s {
+    uint64_t seed;
+    int dist;
+    int64_t n2;
+    int64_t r;
+    int mode;
+    int omega_transform;
+    int split_override;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sk_status_t fail(sk_status_t st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+sk_status_t cuda_fail(cudaError_t e, const char* where) {
+    return fail(SK_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2D fp32 row-major tensor [rows x cols] with row stride ld (elements), box {box_cols, box_rows},
+// SWIZZLE_128B, out-of-bounds elements read as zero.
+sk_status_t make_map_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols,
+                        int64_t ld, uint32_t box_cols, uint32_t box_rows) {
+    auto enc = get_encode();
+    if (!enc) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(r) + ")");
+    return SK_SUCCESS;
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------- launch planning
+struct SketchPlan {
+    int npass;         // column passes of <= 256 columns
+    int npad[32];      // MMA N per pass
+    int nacc;
+    int a_stages, o_stages;
+    int split;
+    int kiters;
+    int num_mblk;
+    int grid;
+    size_t smem;
+    size_t ws_per_split;  // bytes of one split partial (n1 x npad_max)
+};
+
+SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, size_t ws_cap) {
+    SketchPlan P{};
+    const int64_t rpad = round_up(h->r, 16);
+    P.npass = static_cast<int>((rpad + 255) / 256);
+    int npad_max = 0;
+    for (int i = 0; i < P.npass; ++i) {
+        P.npad[i] = static_cast<int>(std::min<int64_t>(256, rpad - 256 * i));
+        npad_max = std::max(npad_max, P.npad[i]);
+    }
+    P.nacc = (n1 > 128) ? 2 : 1;
+    P.o_stages = 2;
+    const int budget = sk::sketch_gemm_max_smem() - 2048;
+    const int a_stage = P.nacc * 128 * 32 * 4;
+    P.a_stages = std::min(6, (budget - P.o_stages * npad_max * 128) / a_stage);
+    P.smem = sk::sketch_gemm_smem_bytes(P.nacc, npad_max, P.a_stages, P.o_stages);
+    P.kiters = static_cast<int>((k + kshift + 31) / 32);
+    P.num_mblk = static_cast<int>((n1 + 128 * P.nacc - 1) / (128 * P.nacc));
+    P.ws_per_split = static_cast<size_t>(n1) * npad_max * sizeof(float);
+    const int nsm = sk::num_sms();
+    int best_s = 1;
+    if (h->split_override > 0) {
+        best_s = std::min(h->split_override, std::max(1, P.kiters));
+    } else {
+        double best = 1e300;
+        const double unit_ovh = 2.0;  // epilogue + pipeline fill, in K-iteration units
+        for (int s = 1; s <= std::min(64, std::max(1, P.kiters / 4)); ++s) {
+            const int64_t units = static_cast<int64_t>(P.num_mblk) * s;
+            const int64_t waves = (units + nsm - 1) / nsm;
+            const int kper = (P.kiters + s - 1) / s;
+            double t = static_cast<double>(waves) * (kper + unit_ovh);
+            if (s > 1)
+                t += static_cast<double>(s + 1) * n1 * npad_max * 4.0 /
+                     (static_cast<double>(nsm) * a_stage);
+            if (t < best * 0.995) { best = t; best_s = s; }
+        }
+    }
+    if (best_s > 1 && ws_cap < static_cast<size_t>(best_s) * P.ws_per_split)
+        best_s = std::max<int>(1, static_cast<int>(ws_cap / P.ws_per_split));
+    // each split must own >= 1 K iteration
+    const int kper = (P.kiters + best_s - 1) / best_s;
+    P.split = (P.kiters + kper - 1) / kper;
+    const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
+    P.grid = static_cast<int>(std::min<int64_t>(units, nsm));
+    return P;
+}
+
+size_t sketch_ws_bytes(const sk_sketch_s* h, int64_t n1, int64_t k) {
+    const SketchPlan P = plan_sketch(h, n1, k, 127, ~size_t(0));
+    return P.split > 1 ? P.split * P.ws_per_split : 0;
+}
+
+struct CorePlan {
+    int chunks;
+    int chunk_rows;
+};
+
+CorePlan plan_core(const sk_sketch_s* h, int64_t m) {
+    CorePlan C{};
+    const int64_t tiles = ((h->r + 63) / 64) * ((h->r + 63) / 64);
+    const int64_t want = std::max<int64_t>(1, (2 * sk::num_sms() + tiles - 1) / tiles);
+    const int64_t maxc = std::max<int64_t>(1, (m + 31) / 32);
+    const int64_t chunks = std::min(want, maxc);
+    C.chunk_rows = static_cast<int>(round_up((m + chunks - 1) / chunks, 32));
+    C.chunks = static_cast<int>((m + C.chunk_rows - 1) / C.chunk_rows);
+    return C;
+}
+
+size_t core_ws_bytes(const sk_sketch_s* h, int64_t m) {
+    const CorePlan C = plan_core(h, m);
+    return static_cast<size_t>(C.chunks) * h->r * h->r * sizeof(float);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+sk_status_t check_handle(const sk_sketch_s* h) {
+    if (!h) return fail(SK_ERR_INVALID_VALUE, "NULL handle");
+    return SK_SUCCESS;
+}
+
+sk_status_t check_mode(const sk_sketch_s* h) {
+    if (h->mode != sk::kTF32)
+        return fail(SK_ERR_UNSUPPORTED, "this build implements SK_MODE_TF32 only");
+    if (h->omega_transform == SK_OMEGA_FAST && h->mode == sk::kTF32x3)
+        return fail(SK_ERR_UNSUPPORTED, "SK_OMEGA_FAST is not allowed with SK_MODE_TF32X3");
+    return SK_SUCCESS;
+}
+
+// B_part[m x r] = A[m x k] * Omega[k0 : k0+k, :r]
+sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int64_t lda,
+                       int64_t k0, float* B, int64_t ldb, void* ws, size_t ws_bytes,
+                       cudaStream_t stream) {
+    if (m == 0) return SK_SUCCESS;
+    // Omega tile rows start at a 128-aligned global row (+ roff = k0 % 4); the matching A columns
+    // start kshift (a multiple of 4) columns left of column 0 and are zero-filled by TMA.
+    const int kshift = static_cast<int>(k0 & 124);
+    const int roff = static_cast<int>(k0 & 3);
+    const SketchPlan P = plan_sketch(h, m, k, kshift, ws_bytes);
+    CUtensorMap map;
+    sk_status_t st = make_map_2d(&map, A, m, k, lda, 32, 128);
+    if (st != SK_SUCCESS) return st;
+    for (int pass = 0; pass < P.npass; ++pass) {
+        sk::SketchGemmParams p{};
+        const int c0 = 256 * pass;
+        p.r_valid = static_cast<int32_t>(std::min<int64_t>(h->r - c0, P.npad[pass]));
+        p.npad = P.npad[pass];
+        p.c0 = c0;
+        p.k0a = k0 - kshift;
+        p.kshift = kshift;
+        p.roff = roff;
+        p.n1 = static_cast<int32_t>(m);
+        p.kiters = P.kiters;
+        p.num_mblk = P.num_mblk;
+        p.split = P.split;
+        p.kper = (P.kiters + P.split - 1) / P.split;
+        p.a_stages = P.a_stages;
+        p.o_stages = P.o_stages;
+        p.key0 = static_cast<uint32_t>(h->seed);
+        p.key1 = static_cast<uint32_t>(h->seed >> 32);
+        if (P.split > 1) {
+            p.out = static_cast<float*>(ws);
+            p.ldo = p.npad;
+            p.part_stride = m * static_cast<int64_t>(p.npad);
+        } else {
+            p.out = B + c0;
+            p.ldo = ldb;
+            p.part_stride = 0;
+        }
+        cudaError_t e = sk::launch_sketch_gemm(map, p, P.nacc, h->dist, h->mode,
+                                               h->omega_transform == SK_OMEGA_FAST, P.grid,
+                                               P.smem, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
+        if (P.split > 1) {
+            e = sk::launch_splitk_reduce(static_cast<const float*>(ws), p.part_stride, P.split,
+                                         p.n1, p.r_valid, p.npad, B + c0, ldb, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
+        }
+    }
+    return SK_SUCCESS;
+}
+
+// C[r x r] (ldc) = Omega[i0 : i0+m, :r]^T * B[m x r]
+sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, int64_t i0,
+                      float* C, int64_t ldc, void* ws, cudaStream_t stream) {
+    const CorePlan CP = plan_core(h, m);
+    sk::CoreGemmParams p{};
+    p.B = B;
+    p.ldb = ldb;
+    p.part = static_cast<float*>(ws);
+    p.ldp = h->r;
+    p.i0 = i0;
+    p.m = static_cast<int32_t>(m);
+    p.r = static_cast<int32_t>(h->r);
+    p.chunk_rows = CP.chunk_rows;
+    p.chunks = CP.chunks;
+    p.key0 = static_cast<uint32_t>(h->seed);
+    p.key1 = static_cast<uint32_t>(h->seed >> 32);
+    if (m == 0) {
+        cudaError_t e = cudaMemset2DAsync(C, ldc * sizeof(float), 0, h->r * sizeof(float), h->r, stream);
+        return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "memset C");
+    }
+    cudaError_t e = sk::launch_core_gemm(p, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "core_gemm launch");
+    e = sk::launch_core_reduce(p.part, p.chunks, p.r, C, ldc, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "core_reduce launch");
+    return SK_SUCCESS;
+}
+
+}  // namespace
+
+namespace sk {
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+    }
+    return n;
+}
+}  // namespace sk
+
+extern "C" {
+
+sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, sk_sketch_t* out) {
+    if (!out) return fail(SK_ERR_INVALID_VALUE, "out == NULL");
+    if (n2 < 1) return fail(SK_ERR_INVALID_VALUE, "n2 must be >= 1");
+    if (r < 1 || r > 4096) return fail(SK_ERR_INVALID_VALUE, "r must be in [1, 4096]");
+    if (dist != SK_DIST_GAUSSIAN && dist != SK_DIST_RADEMACHER && dist != SK_DIST_UNIFORM)
+        return fail(SK_ERR_INVALID_VALUE, "unknown distribution");
+    auto* h = new (std::nothrow) sk_sketch_s{seed, static_cast<int>(dist), n2, r, sk::kTF32,
+                                             SK_OMEGA_ACCURATE, 0};
+    if (!h) return fail(SK_ERR_INVALID_VALUE, "out of host memory");
+    *out = h;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_destroy(sk_sketch_t h) {
+    delete h;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_mode(sk_sketch_t h, sk_mode_t mode) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (mode != SK_MODE_TF32X3 && mode != SK_MODE_TF32 && mode != SK_MODE_BF16)
+        return fail(SK_ERR_INVALID_VALUE, "unknown mode");
+    h->mode = static_cast<int>(mode);
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_omega_transform(sk_sketch_t h, sk_omega_transform_t t) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (t != SK_OMEGA_ACCURATE && t != SK_OMEGA_FAST)
+        return fail(SK_ERR_INVALID_VALUE, "unknown omega transform");
+    h->omega_transform = static_cast<int>(t);
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (split_k < 0 || split_k > 64) return fail(SK_ERR_INVALID_VALUE, "split_k must be in [0, 64]");
+    h->split_override = split_k;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_workspace_size(sk_sketch_t h, int64_t n1, size_t* bytes) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (!bytes || n1 < 0) return fail(SK_ERR_INVALID_VALUE, "bad workspace query");
+    *bytes = std::max(sketch_ws_bytes(h, n1, h->n2), core_ws_bytes(h, std::max<int64_t>(n1, 1)));
+    return SK_SUCCESS;
+}
+
+static sk_status_t validate_apply(sk_sketch_t h, const float* A, int64_t m, int64_t k, int64_t lda,
+                                  int64_t k0, const float* B, int64_t ldb, void* ws,
+                                  size_t ws_bytes) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (sk_status_t st = check_mode(h)) return st;
+    if (m < 0 || k < 1) return fail(SK_ERR_INVALID_VALUE, "need m >= 0 and k >= 1");
+    if (m > (1ll << 31) - 256) return fail(SK_ERR_UNSUPPORTED, "m >= 2^31 rows");
+    if (k0 < 0 || k0 + k > h->n2)
+        return fail(SK_ERR_SHAPE_MISMATCH, "Omega rows [k0, k0+k) exceed the handle's n2");
+    if (m > 0 && (!A || !B)) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if (lda < k) return fail(SK_ERR_SHAPE_MISMATCH, "lda < number of columns of A");
+    if (ldb < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "ldb < r");
+    if (!aligned16(A) || (lda & 3)) return fail(SK_ERR_ALIGNMENT, "A must be 16-byte aligned with lda % 4 == 0");
+    size_t need = 0;
+    sketch_workspace_size(h, m, &need);
+    if (ws_bytes < need || (need > 0 && !ws))
+        return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_workspace_size (" +
+                                          std::to_string(need) + " bytes)");
+    if (ws && !aligned16(ws)) return fail(SK_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_apply(sk_sketch_t h, const float* A, int64_t n1, int64_t n2, int64_t lda,
+                         float* B, int64_t ldb, void* ws, size_t ws_bytes, void* stream) {
+    if (h && n2 != h->n2) return fail(SK_ERR_SHAPE_MISMATCH, "n2 != handle n2");
+    if (sk_status_t st = validate_apply(h, A, n1, n2, lda, 0, B, ldb, ws, ws_bytes)) return st;
+    return apply_impl(h, A, n1, n2, lda, 0, B, ldb, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t sketch_apply_block(sk_sketch_t h, const float* A_blk, int64_t m, int64_t k,
+                               int64_t lda, int64_t k0, float* B_part, int64_t ldb, void* ws,
+                               size_t ws_bytes, void* stream) {
+    if (sk_status_t st = validate_apply(h, A_blk, m, k, lda, k0, B_part, ldb, ws, ws_bytes)) return st;
+    return apply_impl(h, A_blk, m, k, lda, k0, B_part, ldb, ws, ws_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb,
+                             int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
+                             void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (sk_status_t st = check_mode(h)) return st;
+    if (m < 0 || i0 < 0 || i0 + m > h->n2)
+        return fail(SK_ERR_SHAPE_MISMATCH, "Omega rows [i0, i0+m) exceed the handle's n2");
+    if ((m > 0 && !B_blk) || !C_part) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if (ldb < h->r || ldc < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "ldb / ldc < r");
+    const size_t need = core_ws_bytes(h, std::max<int64_t>(m, 1));
+    if (ws_bytes < need || !ws)
+        return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_workspace_size");
+    return core_impl(h, B_blk, m, ldb, i0, C_part, ldc, ws, static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t nystrom_core(sk_sketch_t h, const float* A, int64_t n, int64_t lda, float* B,
+                         int64_t ldb, float* C, int64_t ldc, void* ws, size_t ws_bytes,
+                         void* stream) {
+    if (h && n != h->n2) return fail(SK_ERR_SHAPE_MISMATCH, "n != handle n2 (A must be n2 x n2)");
+    if (sk_status_t st = validate_apply(h, A, n, n, lda, 0, B, ldb, ws, ws_bytes)) return st;
+    if (!C) return fail(SK_ERR_INVALID_VALUE, "NULL C");
+    if (ldc < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "ldc < r");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (sk_status_t st = apply_impl(h, A, n, n, lda, 0, B, ldb, ws, ws_bytes, s)) return st;
+    return core_impl(h, B, n, ldb, 0, C, ldc, ws, s);
+}
+
+sk_status_t sketch_generate(sk_sketch_t h, int64_t row0, int64_t nrows, int64_t col0,
+                            int64_t ncols, float* out, int64_t ld, void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (!out || row0 < 0 || nrows < 0 || col0 < 0 || ncols < 0 || col0 + ncols > h->r ||
+        row0 + nrows > (1ll << 62) || ld < ncols)
+        return fail(SK_ERR_INVALID_VALUE, "block outside [0, 2^62) x [0, r) or bad ld");
+    cudaError_t e = sk::launch_generate(h->seed, h->dist, row0, nrows, col0, ncols, out, ld, false,
+                                        static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "generate launch");
+}
+
+sk_status_t sketch_generate_bits(sk_sketch_t h, int64_t row0, int64_t nrows, int64_t col0,
+                                 int64_t ncols, uint32_t* out, int64_t ld, void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (!out || row0 < 0 || nrows < 0 || col0 < 0 || ncols < 0 || col0 + ncols > h->r ||
+        row0 + nrows > (1ll << 62) || ld < ncols)
+        return fail(SK_ERR_INVALID_VALUE, "block outside [0, 2^62) x [0, r) or bad ld");
+    cudaError_t e = sk::launch_generate(h->seed, h->dist, row0, nrows, col0, ncols, out, ld, true,
+                                        static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "generate_bits launch");
+}
+
+sk_status_t sketch_debug_box_muller(const uint32_t* w1, const uint32_t* w2, int64_t n,
+                                    sk_omega_transform_t transform, float* out_even,
+                                    float* out_odd, void* stream) {
+    if (n < 0 || (n > 0 && (!w1 || !w2 || !out_even || !out_odd)))
+        return fail(SK_ERR_INVALID_VALUE, "bad debug_box_muller arguments");
+    cudaError_t e = sk::launch_debug_box_muller(w1, w2, n, transform == SK_OMEGA_FAST, out_even,
+                                                out_odd, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "debug_box_muller launch");
+}
+
+const char* sketch_status_string(sk_status_t st) {
+    switch (st) {
+        case SK_SUCCESS: return "SK_SUCCESS";
+        case SK_ERR_INVALID_VALUE: return "SK_ERR_INVALID_VALUE";
+        case SK_ERR_SHAPE_MISMATCH: return "SK_ERR_SHAPE_MISMATCH";
+        case SK_ERR_ALIGNMENT: return "SK_ERR_ALIGNMENT";
+        case SK_ERR_UNSUPPORTED: return "SK_ERR_UNSUPPORTED";
+        case SK_ERR_WORKSPACE: return "SK_ERR_WORKSPACE";
+        case SK_ERR_CUDA: return "SK_ERR_CUDA";
+        case SK_ERR_NCCL: return "SK_ERR_NCCL";
+    }
+    return "SK_ERR_UNKNOWN";
+}
+
+const char* sketch_last_error(void) { return g_last_error.c_str(); }
+
+const char* sketch_build_info(void) {
+    return "libsketch sm_100a (tcgen05 tf32 sketch GEMM, SIMT core GEMM v1)";
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// kernels.cuh -- launch-side declarations shared by the kernels and the C ABI (api.cu).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace sk {
+
+enum Dist : int { kGaussian = 0, kRademacher = 1, kUniform = 2 };
+enum Mode : int { kTF32x3 = 0, kTF32 = 1, kBF16 = 2 };
+
+// One launch of the fused sketch GEMM: B_pass = A[:, kshift-aligned K range] * Omega tile,
+// for accumulator columns [c0, c0 + npad) of Omega.
+struct SketchGemmParams {
+    float* out;           // B (split == 1) or split-K partials (split > 1)
+    int64_t ldo;          // row stride of out (elements)
+    int64_t part_stride;  // elements between consecutive split partials
+    int64_t k0a;          // global Omega row of tile row 0 of K-iteration 0 (= aligned + roff)
+    int32_t kshift;       // A column of tile row 0 is (kit*32 - kshift), kshift % 4 == 0 (TMA
+                          // needs 16-byte inner coordinates); negative columns -> TMA zero fill
+    int32_t roff;         // k0a % 4 (0 except for unaligned block calls)
+    int32_t n1;           // rows of A
+    int32_t kiters;       // number of 32-wide K iterations
+    int32_t r_valid;      // columns of this pass to store (<= npad)
+    int32_t c0;           // global Omega column of accumulator column 0
+    int32_t npad;         // MMA N (multiple of 16, <= 256)
+    int32_t num_mblk;     // ceil(n1 / (128 * nacc))
+    int32_t split;        // split-K factor S
+    int32_t kper;         // K iterations per split
+    int32_t a_stages;     // A smem pipeline depth
+    int32_t o_stages;     // Omega smem pipeline depth
+    uint32_t key0, key1;  // Philox key = (seed lo, seed hi)
+};
+
+struct CoreGemmParams {
+    const float* B;       // B block (m x r, ldb), device
+    int64_t ldb;
+    float* part;          // per-chunk r x r partials (chunks x r x r), or C if chunks == 1
+    int64_t ldp;          // row stride of a partial (elements)
+    int64_t i0;           // global Omega row of B row 0
+    int32_t m;            // rows of B
+    int32_t r;
+    int32_t chunk_rows;   // rows of B per CTA chunk
+    int32_t chunks;
+    uint32_t key0, key1;
+};
+
+struct LaunchCfg {
+    int nacc;
+    int split;
+    int grid;
+    int a_stages;
+    int o_stages;
+    size_t smem;
+};
+
+// Host-side launchers (return cudaError_t of the launch).
+cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int nacc,
+                               int dist, int mode, bool fast, int grid, size_t smem,
+                               cudaStream_t s);
+size_t sketch_gemm_smem_bytes(int nacc, int npad, int a_stages, int o_stages);
+int sketch_gemm_max_smem();
+
+cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,
+                                 int32_t n1, int32_t r_valid, int32_t ldp, float* out,
+                                 int64_t ldo, cudaStream_t s);
+
+cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaStream_t s);
+cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
+                               int64_t ldc, cudaStream_t s);
+
+cudaError_t launch_generate(uint64_t seed, int dist, int64_t row0, int64_t nrows, int64_t col0,
+                            int64_t ncols, void* out, int64_t ld, bool bits, cudaStream_t s);
+cudaError_t launch_debug_box_muller(const uint32_t* w1, const uint32_t* w2, int64_t n, bool fast,
+                                    float* oe, float* oo, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace sk

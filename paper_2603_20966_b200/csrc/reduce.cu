@@ -1,0 +1,84 @@
+// reduce.cu -- deterministic fixed-order reductions (reading R9): split-K partials of B and
+// per-chunk r x r partials of C.  Partial s is always added in increasing s.
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace sk {
+
+// out[i, c] = sum_{s < split} part[s][i][c]   (part row stride ldp, s stride part_stride)
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t part_stride,
+                                     int32_t split, int32_t n1, int32_t r_valid, int32_t ldp,
+                                     float* __restrict__ out, int64_t ldo) {
+    const int64_t total = static_cast<int64_t>(n1) * r_valid;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / r_valid;
+        const int64_t c = idx - i * r_valid;
+        const float* p = part + i * ldp + c;
+        float acc = __ldg(p);
+        for (int s = 1; s < split; ++s) acc += __ldg(p + s * part_stride);
+        out[i * ldo + c] = acc;
+    }
+}
+
+// Vectorised variant: 4 consecutive columns per thread (r_valid % 4 == 0, aligned rows).
+__global__ void splitk_reduce_kernel_v4(const float4* __restrict__ part, int64_t part_stride4,
+                                        int32_t split, int32_t n1, int32_t r4, int32_t ldp4,
+                                        float4* __restrict__ out, int64_t ldo4) {
+    const int64_t total = static_cast<int64_t>(n1) * r4;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / r4;
+        const int64_t c = idx - i * r4;
+        const float4* p = part + i * ldp4 + c;
+        float4 acc = __ldg(p);
+        for (int s = 1; s < split; ++s) {
+            const float4 v = __ldg(p + s * part_stride4);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        out[i * ldo4 + c] = acc;
+    }
+}
+
+cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,
+                                 int32_t n1, int32_t r_valid, int32_t ldp, float* out,
+                                 int64_t ldo, cudaStream_t s) {
+    if (n1 <= 0 || r_valid <= 0) return cudaSuccess;
+    const int threads = 256;
+    const bool v4 = (r_valid % 4 == 0) && (ldp % 4 == 0) && (ldo % 4 == 0) &&
+                    (part_stride % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(part) & 15) == 0);
+    const int64_t total = static_cast<int64_t>(n1) * (v4 ? r_valid / 4 : r_valid);
+    const int blocks = static_cast<int>(std::min<int64_t>((total + threads - 1) / threads, 148 * 16));
+    if (v4)
+        splitk_reduce_kernel_v4<<<blocks, threads, 0, s>>>(
+            reinterpret_cast<const float4*>(part), part_stride / 4, split, n1, r_valid / 4,
+            ldp / 4, reinterpret_cast<float4*>(out), ldo / 4);
+    else
+        splitk_reduce_kernel<<<blocks, threads, 0, s>>>(part, part_stride, split, n1, r_valid,
+                                                        ldp, out, ldo);
+    return cudaGetLastError();
+}
+
+// C[a, b] = sum_{c < chunks} part[c][a][b], r x r, fixed order.
+__global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r,
+                                   float* __restrict__ C, int64_t ldc) {
+    const int64_t rr = static_cast<int64_t>(r) * r;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < rr;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int c = 0; c < chunks; ++c) acc += __ldg(part + c * rr + idx);
+        C[(idx / r) * ldc + idx % r] = acc;
+    }
+}
+
+cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
+                               int64_t ldc, cudaStream_t s) {
+    const int64_t rr = static_cast<int64_t>(r) * r;
+    const int blocks = static_cast<int>(std::min<int64_t>((rr + 255) / 256, 148 * 8));
+    core_reduce_kernel<<<blocks, 256, 0, s>>>(part, chunks, r, C, ldc);
+    return cudaGetLastError();
+}
+
+}  // namespace sk

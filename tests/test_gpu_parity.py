@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Tolerances (north star):
+  Omega words / Rademacher signs / uniforms: bit-exact;  Gaussians: <= 2 ulp (accurate transform);
+  B, C: relF <= 5e-3 in tf32 / bf16 modes, <= 1e-5 in tf32x3; bit-exact in the integer regime
+  (A in {-4..4}, Rademacher Omega: every partial sum is an exact fp32 integer, any order).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SEED = 42
+
+
+def _sk():
+    import paper_2603_20966_b200 as sk
+    return sk
+
+
+def _relF(x, ref):
+    x = np.asarray(x, np.float64)
+    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+def _ulp(a, b):
+    """ulp distance between fp32 arrays, +0 == -0."""
+    def ordered(x):
+        i = np.asarray(x, np.float32).view(np.int32).astype(np.int64)
+        return np.where(i < 0, -(i & 0x7FFFFFFF), i)
+    return np.abs(ordered(a) - ordered(b))
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+TOL = {"tf32": 5e-3, "bf16": 5e-3, "tf32x3": 1e-5}
+
+
+# ----------------------------------------------------------------------------- Omega
+@pytest.mark.parametrize("dist", ["gaussian", "rademacher", "uniform"])
+@pytest.mark.parametrize("block", [(0, 64, 0, 16), (3, 130, 5, 9), (1000, 257, 0, 33), (2**33 + 1, 40, 2, 7)])
+def test_generate_bits_exact(dist, block):
+    sk = _sk()
+    row0, nrows, col0, ncols = block
+    s = sk.Sketch(SEED, dist, 2**40, 48)
+    got = s.generate_bits(row0, nrows, col0, ncols).cpu().numpy().view(np.uint32)
+    ref = oracle.omega_words(SEED, dist, row0, nrows, col0, ncols)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("dist", ["rademacher", "uniform"])
+def test_generate_values_exact(dist):
+    sk = _sk()
+    s = sk.Sketch(7, dist, 10**6, 40)
+    got = s.generate(77, 1000, 0, 40).cpu().numpy()
+    assert np.array_equal(got, oracle.omega(7, dist, 77, 1000, 0, 40))
+
+
+def test_generate_gaussian_ulp():
+    sk = _sk()
+    s = sk.Sketch(SEED, "gaussian", 10**7, 64)
+    got = s.generate(5, 4096, 0, 64).cpu().numpy()
+    ref = oracle.omega(SEED, "gaussian", 5, 4096, 0, 64)
+    assert _ulp(got, ref).max() <= 2
+
+
+@pytest.mark.parametrize("transform", ["accurate"])
+def test_box_muller_ulp_sweeps(transform):
+    """Every u1 (radius sweep, u2 = 0 so z_even = R exactly) and every u2 at fixed u1s."""
+    sk = _sk()
+    n = 1 << 24
+    w1 = (np.arange(n, dtype=np.uint64) << 8).astype(np.uint32)
+    w2 = np.zeros(n, dtype=np.uint32)
+    ge, go = sk.debug_box_muller(_dev(w1.view(np.int32)), _dev(w2.view(np.int32)), transform)
+    re_, ro = oracle.box_muller_many(w1, w2)
+    assert _ulp(ge.cpu().numpy(), re_).max() <= 2
+    assert np.all(go.cpu().numpy() == 0.0)
+    for u1 in (0, 12345, 1 << 23, (1 << 24) - 2):
+        w1c = np.full(n, u1 << 8, dtype=np.uint32)
+        ge, go = sk.debug_box_muller(_dev(w1c.view(np.int32)), _dev(w1.view(np.int32)), transform)
+        re_, ro = oracle.box_muller_many(w1c, w1)
+        assert _ulp(ge.cpu().numpy(), re_).max() <= 2
+        assert _ulp(go.cpu().numpy(), ro).max() <= 2
+
+
+def test_box_muller_fast_close():
+    """Fast (MUFU) transform: error <= 2^-16 * max(|z|, 1) on random pairs (reading R5: far below
+    the 2^-11 tf32 / 2^-8 bf16 operand rounding it is allowed under)."""
+    sk = _sk()
+    rng = np.random.default_rng(0)
+    n = 1 << 22
+    w1 = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    w2 = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    ge, go = sk.debug_box_muller(_dev(w1.view(np.int32)), _dev(w2.view(np.int32)), "fast")
+    re_, ro = oracle.box_muller_many(w1, w2)
+    for g, r in ((ge.cpu().numpy(), re_), (go.cpu().numpy(), ro)):
+        err = np.abs(g.astype(np.float64) - r) / np.maximum(np.abs(r), 1.0)
+        assert err.max() <= 2.0**-16
+
+
+# ----------------------------------------------------------------------------- B = A Omega
+SHAPES = [
+    (512, 512, 16),     # c1
+    (300, 1000, 48),    # ragged M / K / N
+    (129, 33, 17),      # one row past a tile, tiny K
+    (1000, 4099, 256),  # several tiles, ragged K, N = 256
+    (64, 2000, 300),    # two column passes (256 + 44)
+    (2000, 777, 128),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dist", ["gaussian", "rademacher"])
+@pytest.mark.parametrize("mode", ["tf32"])
+def test_sketch_parity(shape, dist, mode):
+    sk = _sk()
+    n1, n2, r = shape
+    A = synth.uniform(1, n1, n2)
+    s = sk.Sketch(SEED, dist, n2, r, mode=mode)
+    B = s.apply(_dev(A)).cpu().numpy()
+    ref = oracle.sketch(SEED, dist, A, r)
+    assert _relF(B, ref) <= TOL[mode]
+
+
+@pytest.mark.parametrize("split", [1, 3, 7])
+def test_sketch_split_k_and_determinism(split):
+    sk = _sk()
+    A = synth.uniform(3, 700, 3000)
+    s = sk.Sketch(SEED, "gaussian", 3000, 64, split_k=split)
+    Ad = _dev(A)
+    B1 = s.apply(Ad)
+    B2 = s.apply(Ad)
+    assert torch.equal(B1, B2)  # fixed-order reductions: bit-identical reruns
+    assert _relF(B1.cpu().numpy(), oracle.sketch(SEED, "gaussian", A, 64)) <= 5e-3
+
+
+@pytest.mark.parametrize("mode", ["tf32"])
+@pytest.mark.parametrize("split", [1, 4])
+def test_sketch_integer_exact(mode, split):
+    sk = _sk()
+    A = synth.int_matrix(5, 777, 1500, -4, 4)
+    s = sk.Sketch(SEED, "rademacher", 1500, 80, mode=mode, split_k=split)
+    B = s.apply(_dev(A)).cpu().numpy()
+    assert np.array_equal(B.astype(np.float64), oracle.sketch(SEED, "rademacher", A, 80))
+
+
+def test_sketch_identity_reproduces_omega():
+    sk = _sk()
+    n = 256
+    s = sk.Sketch(SEED, "rademacher", n, 32)
+    B = s.apply(_dev(np.eye(n, dtype=np.float32))).cpu().numpy()
+    assert np.array_equal(B, oracle.omega(SEED, "rademacher", 0, n, 0, 32))
+
+
+@pytest.mark.parametrize("k0", [0, 1, 100, 128, 333])
+def test_apply_block_offsets(k0):
+    sk = _sk()
+    n2 = 2000
+    A = synth.uniform(9, 300, 700)
+    s = sk.Sketch(SEED, "gaussian", n2, 40)
+    Bp = s.apply_block(_dev(A), k0).cpu().numpy()
+    ref = oracle.sketch(SEED, "gaussian", A, 40, k0=k0)
+    assert _relF(Bp, ref) <= 5e-3
+    si = sk.Sketch(SEED, "rademacher", n2, 40)
+    Ai = synth.int_matrix(9, 300, 700)
+    assert np.array_equal(si.apply_block(_dev(Ai), k0).cpu().numpy().astype(np.float64),
+                          oracle.sketch(SEED, "rademacher", Ai, 40, k0=k0))
+
+
+def test_lda_padding_and_strided_out():
+    sk = _sk()
+    A = synth.uniform(4, 200, 516)
+    Ad = _dev(A)[:, :500]  # lda = 516 > n2 = 500
+    s = sk.Sketch(SEED, "gaussian", 500, 24)
+    out = torch.zeros((200, 40), device="cuda")[:, 3:27]  # ldb = 40, offset output
+    s.apply(Ad, out=out)
+    assert _relF(out.cpu().numpy(), oracle.sketch(SEED, "gaussian", A[:, :500], 24)) <= 5e-3
+
+
+# ----------------------------------------------------------------------------- C = Omega^T B
+@pytest.mark.parametrize("n,r", [(512, 16), (1000, 64), (777, 100), (2048, 256)])
+def test_nystrom_core_parity(n, r):
+    sk = _sk()
+    A = synth.symmetric_uniform(6, n)
+    s = sk.Sketch(SEED, "gaussian", n, r)
+    B, C = s.nystrom_core(_dev(A))
+    Bref, Cref = oracle.nystrom_core(SEED, "gaussian", A, r)
+    assert _relF(B.cpu().numpy(), Bref) <= 5e-3
+    assert _relF(C.cpu().numpy(), Cref) <= 5e-3
+    # C against the oracle core applied to the GPU's own B isolates the core GEMM (fp32 SIMT)
+    Cown = oracle.core(SEED, "gaussian", B.cpu().numpy().astype(np.float64))
+    assert _relF(C.cpu().numpy(), Cown) <= 1e-5
+
+
+def test_nystrom_core_integer_exact():
+    sk = _sk()
+    A, X = synth.lowrank_psd(3, 1024, 8, -2, 2)
+    s = sk.Sketch(SEED, "rademacher", 1024, 64)
+    B, C = s.nystrom_core(_dev(A))
+    Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, 64)
+    assert np.array_equal(B.cpu().numpy().astype(np.float64), Bref)
+    assert np.array_equal(C.cpu().numpy().astype(np.float64), Cref)
+    assert torch.equal(C, C.T)
+
+
+@pytest.mark.parametrize("i0", [0, 5, 130])
+def test_core_block(i0):
+    sk = _sk()
+    Bm = synth.uniform(8, 500, 48).astype(np.float32)
+    s = sk.Sketch(SEED, "gaussian", 1000, 48)
+    Cp = s.core_block(_dev(Bm), i0).cpu().numpy()
+    assert _relF(Cp, oracle.core(SEED, "gaussian", Bm.astype(np.float64), i0=i0)) <= 1e-5
+
+
+# ----------------------------------------------------------------------------- errors
+def test_error_codes():
+    sk = _sk()
+    s = sk.Sketch(SEED, "gaussian", 100, 8)
+    A = torch.zeros((10, 100), device="cuda")
+    with pytest.raises(sk.SketchError) as e:
+        s.apply(torch.zeros((10, 99), device="cuda"))
+    assert e.value.name == "SK_ERR_SHAPE_MISMATCH"
+    lib = sk.load_library()
+    Am = torch.zeros((10, 103), device="cuda")[:, 1:101]
+    ws = s.workspace(10)
+    Bm = torch.empty((10, 8), device="cuda")
+    st = lib.sketch_apply(s._h, Am.data_ptr(), 10, 100, 103, Bm.data_ptr(), 8, ws.data_ptr(), ws.numel() * 4, None)
+    assert lib.sketch_status_string(st) == b"SK_ERR_ALIGNMENT"
+    # the binding realigns such inputs (one copy) instead of failing
+    assert s.apply(Am).abs().max().item() == 0.0
+    with pytest.raises(sk.SketchError) as e:
+        s.generate(0, 4, 5, 8)
+    assert e.value.name == "SK_ERR_INVALID_VALUE"
+    assert s.apply(A).abs().max().item() == 0.0
+    assert s.apply(torch.zeros((0, 100), device="cuda")).shape == (0, 8)
