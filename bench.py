@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""bench.py -- the sketch B = A*Omega + Nystrom core C = Omega^T*B on B200 (BASELINE.json metric).
+
+Default workload (N = 1): BASELINE.json configs[1] = c2, the Nystrom core of a symmetric PSD
+n = 50,000 matrix (synthetic RBF kernel of X ~ U[0,1)^{50000 x 3072}, the CIFAR-10-shaped
+analogue of PAPER.md:1013-1024), r = 256 Gaussian Omega regenerated in-kernel.  One step = one
+full pass of the hot path: B = A Omega (fused Omega tiles + tcgen05 GEMM [+ split-K reduce]) and
+C = Omega^T B (Omega regenerated) [+ AllReduce of C for N > 1].
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--mode tf32]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (row-block layout by default)
+  python bench.py --impl reference ...                    (the fp64 CPU oracle on host cores)
+
+Prints ONE JSON line (rank 0).  value = effective GB/s of A over the whole job (all ranks' A
+bytes / max-over-ranks device time); TFLOP/s, per-phase device times, roofline of the dominant
+kernel, the oracle baseline, e2e (host buffers), clocks and launch counts ride along.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketch A·Ω effective HBM GB/s + TFLOP/s (% roofline) at 1/2/4/8 B200; Nyström core time"
+
+WORKLOADS = {
+    "c1": dict(desc="c1: A 512x512 symmetric fp32, Gaussian Omega r=16, B=A*Omega and C=Omega^T*B",
+               n1=512, n2=512, r=16, dist="gaussian", nystrom=True, a="symuniform"),
+    "c2": dict(desc="c2: Nystrom core, symmetric PSD A n=50,000 (RBF kernel of X~U[0,1)^{50000x3072}), "
+                    "r=256 Gaussian",
+               n1=50000, n2=50000, r=256, dist="gaussian", nystrom=True, a="rbf", d=3072),
+    "c3": dict(desc="c3: tall-skinny A 4,000,000x2,048 fp32 U[-1/2,1/2), r=128 Rademacher, row-block",
+               n1=4_000_000, n2=2048, r=128, dist="rademacher", nystrom=False, a="uniform"),
+    "c4": dict(desc="c4: short-wide A 2,048x4,000,000 fp32 U[-1/2,1/2), r=512 Gaussian",
+               n1=2048, n2=4_000_000, r=512, dist="gaussian", nystrom=False, a="uniform"),
+}
+
+SEED_OMEGA = 42
+SEED_A = {"c1": 1, "c2": 2, "c3": 3, "c4": 4}
+NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200 dense tensor peaks (B200_PROFILING.md nominal table)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
+                    bf16_sus=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                    source="MEASURED_PEAKS.json (measured)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="B200_PROFILING.md fallback")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + clock-event reasons through NVML while the timed region runs."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[device_index]) if vis else device_index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            log(f"[bench] NVML unavailable: {e}")
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self) -> dict:
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"], "samples": 0}
+        self._stop.set()
+        self._t.join()
+        loaded = [s for s in self.samples]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(loaded)}
+
+
+# ----------------------------------------------------------------------------- inputs
+def make_A_block(W, wl_name, r0, r1, c0, c1, device):
+    """Rows [r0,r1) x cols [c0,c1) of the workload's A, generated in HBM (seeded)."""
+    import torch
+    from inputs import synth
+    seed = SEED_A[wl_name]
+    if W["a"] == "rbf":
+        # RBF kernel block: rows r0..r1 of exp(-|x_i - x_j|^2 / 2 sigma^2), X ~ U[0,1)^{n x d}
+        n, d = W["n1"], W["d"]
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        X = torch.rand((n, d), generator=g, device=device, dtype=torch.float64)
+        sigma2 = float((X * X).sum()) / n
+        sq = (X * X).sum(1)
+        out = torch.empty((r1 - r0, c1 - c0), dtype=torch.float32, device=device)
+        step = 4096
+        for i in range(r0, r1, step):
+            ie = min(r1, i + step)
+            d2 = (sq[i:ie, None] + sq[None, c0:c1] - 2.0 * (X[i:ie] @ X[c0:c1].T)).clamp_min_(0.0)
+            out[i - r0:ie - r0] = torch.exp(-d2 / (2.0 * sigma2)).to(torch.float32)
+        del X, sq
+        torch.cuda.empty_cache()
+        return out
+    if W["a"] == "symuniform":
+        A = torch.from_numpy(synth.symmetric_uniform(seed, W["n1"])).to(device)
+        return A[r0:r1, c0:c1].contiguous()
+    # iid U[-1/2, 1/2): generate row blocks with a per-(block) seed so any partition is reproducible
+    out = torch.empty((r1 - r0, c1 - c0), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1_000_003 + r0 * 7 + c0)
+    out.uniform_(-0.5, 0.5, generator=g)
+    return out
+
+
+def host_A_rows(W, wl_name, rows):
+    """Host (numpy) copy of selected rows of A for the CPU oracle -- same recipe, host RNG."""
+    import numpy as np
+    from inputs import synth
+    seed = SEED_A[wl_name]
+    if W["a"] == "rbf":
+        n, d = W["n1"], W["d"]
+        X = np.random.Generator(np.random.PCG64(seed)).random((n, d))
+        sigma2 = float((X * X).sum()) / n
+        sq = (X * X).sum(1)
+        d2 = np.maximum(sq[rows, None] + sq[None, :] - 2.0 * (X[rows] @ X.T), 0.0)
+        return np.exp(-d2 / (2.0 * sigma2)).astype(np.float32)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return (rng.random((len(rows), W["n2"]), dtype=np.float32) - np.float32(0.5)).astype(np.float32)
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def time_oracle(W, A_rows, target_s=12.0, cores=None):
+    """Time the fp64 oracle (as it stands) on a bounded row sample; returns dict + B_sample."""
+    import oracle
+    if cores:
+        oracle.set_num_threads(cores)
+    n_rows = A_rows.shape[0]
+    t0 = time.perf_counter()
+    B = oracle.sketch(SEED_OMEGA, W["dist"], A_rows, W["r"])
+    t = time.perf_counter() - t0
+    return t, B
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, W, wl_name):
+    import numpy as np
+    import oracle
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    oracle.set_num_threads(cores)
+    # calibrate a row sample so that one step takes ~2-4 s of host time
+    probe = 8
+    A = host_A_rows(W, wl_name, list(range(probe)))
+    t0 = time.perf_counter()
+    oracle.sketch(SEED_OMEGA, W["dist"], A, W["r"])
+    tp = time.perf_counter() - t0
+    rows = int(max(8, min(W["n1"], probe * 3.0 / max(tp, 1e-3))))
+    rows = min(rows, 4096)
+    A = host_A_rows(W, wl_name, list(range(rows)))
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        B = oracle.sketch(SEED_OMEGA, W["dist"], A, W["r"])
+        if W["nystrom"]:
+            oracle.core(SEED_OMEGA, W["dist"], B, 0)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    gbs = rows * W["n2"] * 4 / t / 1e9
+    sample = (f"{rows} of {W['n1']} rows of A per step (full K={W['n2']}, r={W['r']}); Omega "
+              f"materialised in fp64 once per call" + ("; + Omega^T B of the sample rows" if W["nystrom"] else ""))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": W["desc"], "sample_rows": rows},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--mode", default="tf32", choices=["tf32", "tf32x3", "bf16"])
+    ap.add_argument("--omega", default="accurate", choices=["accurate", "fast"])
+    ap.add_argument("--layout", default="row", help="row | col | AxB (p1 x p2)")
+    ap.add_argument("--split-k", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    W = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, W, args.workload)
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2603_20966_b200 as sk
+    from paper_2603_20966_b200.dist import DistSketch, Layout, predicted_bytes_per_rank
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    else:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+        tdist.init_process_group("gloo", rank=0, world_size=1)
+    layout = Layout.parse(args.layout, world)
+    n1, n2, r = W["n1"], W["n2"], W["r"]
+    peaks = load_peaks()
+
+    local = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=args.mode, omega=args.omega, split_k=args.split_k)
+    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local)
+    r0, r1, c0, c1 = ds.a_block_range()
+    t_gen = time.perf_counter()
+    A = make_A_block(W, args.workload, r0, r1, c0, c1, dev)
+    torch.cuda.synchronize()
+    log(f"[bench] rank {rank}: A block {tuple(A.shape)} generated in {time.perf_counter() - t_gen:.1f}s")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if W["nystrom"]:
+            return ds.nystrom_core(A)
+        Bp, rows = ds.apply(A)
+        return Bp, rows, None
+
+    def barrier():
+        if world > 1:
+            tdist.barrier(device_ids=[local_rank])
+
+    for _ in range(args.warmup):
+        out = step()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ------------------------------------------------------------------ timed region
+    sampler = ClockSampler(local_rank)
+    local.set_profiling(True)
+    local.profile_read()  # clear
+    launches0 = sk.launch_count()
+    ds.comm_bytes = 0
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = sk.launch_count() - launches0
+    phases = local.profile_read()
+    local.set_profiling(False)
+    t_ms = e0.elapsed_time(e1)
+    comm_bytes = ds.comm_bytes / args.steps
+    tmax = torch.tensor([t_ms], dtype=torch.float64, device=dev if world > 1 else "cpu")
+    if world > 1:
+        tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
+    t_ms = float(tmax.item())
+    ms_step = t_ms / args.steps
+    a_bytes_total = 4.0 * n1 * n2
+    value = a_bytes_total / (ms_step * 1e-3) / 1e9
+    flops = 2.0 * n1 * n2 * r + (2.0 * n2 * r * r if W["nystrom"] else 0.0)
+    tflops = flops / (ms_step * 1e-3) / 1e12
+
+    # ------------------------------------------------------------------ roofline (dominant kernel)
+    gemm_ms, gemm_launches = phases["sketch_gemm"]
+    m_loc, k_loc = (r1 - r0), (c1 - c0)
+    kern_bytes = 4.0 * m_loc * k_loc + 4.0 * m_loc * r  # A read + B write (algorithmic)
+    kern_flops = 2.0 * m_loc * k_loc * r
+    avg_s = (gemm_ms / max(gemm_launches, 1)) * 1e-3
+    passes = max(1, gemm_launches // max(args.steps, 1))
+    avg_s_step = avg_s * passes  # all column passes of one step
+    tc_peak = {"tf32": peaks["bf16"] * NOMINAL_TF32_OVER_BF16, "tf32x3": peaks["bf16"] * NOMINAL_TF32_OVER_BF16 / 3.0,
+               "bf16": peaks["bf16"]}[args.mode]
+    t_hbm = kern_bytes / (peaks["hbm"] * 1e9)
+    t_tc = kern_flops / (tc_peak * 1e12)
+    if t_hbm >= t_tc:
+        ach = kern_bytes / avg_s_step / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"]}
+    else:
+        ach = kern_flops / avg_s_step / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak}
+    roof.update({
+        "kernel": "sketch_gemm_kernel (fused Philox/Box-Muller Omega tiles + tcgen05 tf32)",
+        "launches_timed": gemm_launches, "avg_launch_ms": avg_s * 1e3,
+        "share_of_step": (gemm_ms / max(t_ms, 1e-9)),
+        "hbm_frac": (kern_bytes / avg_s_step / 1e9) / peaks["hbm"],
+        "tensor_frac": (kern_flops / avg_s_step / 1e12) / tc_peak,
+        "peak_source": peaks["source"] + (", tf32 = bf16 burst x 1.1/2.25 nominal" if args.mode != "bf16" else ", bf16 burst"),
+        "traffic": None,
+    })
+    prof_path = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{args.mode}_{args.omega}.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as f:
+            tr = json.load(f)
+        roof["traffic"] = tr.get("dram_bytes_per_launch")
+        roof["traffic_source"] = os.path.relpath(prof_path, ROOT)
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": args.mode, "data": "synthetic (seeded, generated in HBM)",
+        "config": {"workload": W["desc"], "n1": n1, "n2": n2, "r": r, "dist": W["dist"], "mode": args.mode,
+                   "omega_transform": args.omega, "layout": f"{layout.p1}x{layout.p2}",
+                   "l2": "inputs larger than L2 (A = %.1f GB)" % (a_bytes_total / 1e9) if a_bytes_total > 126e6
+                   else "A fits in L2 (c1: launch-latency bound)"},
+        "tflops": tflops,
+        "nystrom_core_ms": ms_step if W["nystrom"] else None,
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "comm": {"predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"]),
+                 "measured_bytes_per_rank": comm_bytes},
+    }
+
+    # ------------------------------------------------------------------ parity at full size (sampled)
+    if rank == 0 and not args.no_parity:
+        try:
+            import oracle
+            Bp, (a, b), C = out
+            rows = sorted(set(int(x) for x in np.linspace(a, b - 1, 24)))
+            # the exact device rows of A (and, for row-block layouts, all of K) go to the oracle
+            A_rows = A[[x - r0 for x in rows]].cpu().numpy() if (c0, c1) == (0, n2) else None
+            if A_rows is not None:
+                Bref = oracle.sketch(SEED_OMEGA, W["dist"], A_rows, r)
+                Bg = Bp[[x - a for x in rows]].double().cpu().numpy()
+                relB = float(np.linalg.norm(Bg - Bref) / np.linalg.norm(Bref))
+                par = {"rows_sampled": len(rows), "relF_B_rows": relB}
+                if W["nystrom"] and world == 1:
+                    Cown = oracle.core(SEED_OMEGA, W["dist"], Bp.double().cpu().numpy(), 0)
+                    Cg = C.double().cpu().numpy()
+                    par["relF_C_vs_oracle_core_of_gpu_B"] = float(np.linalg.norm(Cg - Cown) / np.linalg.norm(Cown))
+                    par["C_symmetry_relF"] = float(np.linalg.norm(Cg - Cg.T) / np.linalg.norm(Cg))
+                result["parity"] = par
+        except Exception as e:  # pragma: no cover
+            result["parity"] = {"error": repr(e)}
+
+    # ------------------------------------------------------------------ cpu baseline (oracle)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            cores = os.cpu_count()
+            oracle.set_num_threads(cores)
+            probe_rows = A[:8].cpu().numpy()
+            tp, _ = time_oracle(W, probe_rows)
+            nrows = int(max(8, min(A.shape[0], 8 * 12.0 / max(tp, 1e-3))))
+            nrows = min(nrows, 8192)
+            A_rows = A[:nrows].cpu().numpy()
+            t, _ = time_oracle(W, A_rows)
+            result["cpu_baseline"] = {
+                "value": nrows * n2 * 4 / t / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
+                "kind": "oracle",
+                "sample": f"B = A Omega for rows 0..{nrows - 1} of {n1} (full K={n2}, r={r}), fp64, "
+                          f"Omega materialised once; {t:.1f} s",
+            }
+        except Exception as e:  # pragma: no cover
+            result["cpu_baseline"] = {"error": repr(e)}
+
+    # ------------------------------------------------------------------ e2e (host buffers)
+    if not args.no_e2e:
+        try:
+            Ah = torch.empty(A.shape, dtype=torch.float32, pin_memory=True)
+            Ah.copy_(A)
+            Bh = torch.empty((out[0].shape[0], r), dtype=torch.float32, pin_memory=True)
+            Ch = torch.empty((r, r), dtype=torch.float32, pin_memory=True) if W["nystrom"] else None
+            torch.cuda.synchronize()
+            barrier()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(args.e2e_steps):
+                A.copy_(Ah, non_blocking=True)
+                o = step()
+                Bh.copy_(o[0], non_blocking=True)
+                if Ch is not None:
+                    Ch.copy_(o[2], non_blocking=True)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            te = torch.tensor([f0.elapsed_time(f1) / args.e2e_steps], dtype=torch.float64,
+                              device=dev if world > 1 else "cpu")
+            if world > 1:
+                tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+            te = float(te.item())
+            result["e2e"] = {"value": a_bytes_total / (te * 1e-3) / 1e9, "unit": "GB/s",
+                             "h2d_bytes_per_step": int(A.numel() * 4),
+                             "d2h_bytes_per_step": int(Bh.numel() * 4 + (Ch.numel() * 4 if Ch is not None else 0)),
+                             "ms_per_step": te,
+                             "path": "pinned host A -> H2D, nystrom_core/apply via libsketch, D2H of B (and C)"}
+            del Ah
+        except Exception as e:  # pragma: no cover
+            result["e2e"] = {"error": repr(e)}
+
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        tdist.barrier(device_ids=[local_rank])
+    tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

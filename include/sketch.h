@@ -133,6 +133,25 @@ sk_status_t sketch_debug_box_muller(const uint32_t* w1, const uint32_t* w2, int6
                                     sk_omega_transform_t transform, float* out_even,
                                     float* out_odd, void* stream);
 
+/* Phase timing, the analogue of the paper's per-phase timers (genOmegaTime, dgemm1Time, ...,
+ * PAPER.md:1462-1467; Omega generation is fused into the GEMMs here, so it has no phase of its own).
+ * When enabled, every kernel the handle launches is bracketed by CUDA events recorded on the
+ * launch stream.  sketch_profile_read synchronises on the recorded events, writes the summed
+ * device milliseconds and launch counts per phase (arrays of SK_PHASE_COUNT), and clears them. */
+typedef enum {
+    SK_PHASE_SKETCH_GEMM = 0, /* fused Omega-tile generation + tcgen05 A*Omega               */
+    SK_PHASE_SPLITK_REDUCE = 1,
+    SK_PHASE_CORE_GEMM = 2,   /* fused Omega regeneration + Omega^T*B                          */
+    SK_PHASE_CORE_REDUCE = 3,
+    SK_PHASE_GENERATE = 4,    /* sketch_generate / _bits (test path)                           */
+    SK_PHASE_COUNT = 5
+} sk_phase_t;
+sk_status_t sketch_set_profiling(sk_sketch_t h, int enable);
+sk_status_t sketch_profile_read(sk_sketch_t h, double* ms_per_phase, int64_t* launches_per_phase);
+
+/* Number of kernels this library has launched in the process so far (all handles). */
+uint64_t sketch_launch_count(void);
+
 const char* sketch_status_string(sk_status_t st);
 const char* sketch_last_error(void); /* thread-local detail of the last failing call */
 const char* sketch_build_info(void); /* arch / version string baked in at compile time */

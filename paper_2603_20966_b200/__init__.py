@@ -26,8 +26,10 @@ EXPORTED_SYMBOLS = (
     "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
     "sketch_set_split_k", "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "sketch_generate", "sketch_generate_bits",
-    "sketch_debug_box_muller", "sketch_status_string", "sketch_last_error", "sketch_build_info",
+    "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
+    "sketch_status_string", "sketch_last_error", "sketch_build_info",
 )
+PHASES = ("sketch_gemm", "splitk_reduce", "core_gemm", "core_reduce", "generate")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _lib = None
@@ -73,12 +75,16 @@ def load_library(build_if_missing: bool = True):
         lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_generate_bits.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_debug_box_muller.argtypes = [vp, vp, i64, ctypes.c_int, vp, vp, vp]
+        lib.sketch_set_profiling.argtypes = [vp, ctypes.c_int]
+        lib.sketch_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
+        lib.sketch_launch_count.restype = ctypes.c_uint64
         lib.sketch_status_string.argtypes = [ctypes.c_int]
         lib.sketch_status_string.restype = ctypes.c_char_p
         lib.sketch_last_error.restype = ctypes.c_char_p
         lib.sketch_build_info.restype = ctypes.c_char_p
         for name in EXPORTED_SYMBOLS:
-            if name not in ("sketch_status_string", "sketch_last_error", "sketch_build_info"):
+            if name not in ("sketch_status_string", "sketch_last_error", "sketch_build_info",
+                            "sketch_launch_count"):
                 getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -156,6 +162,17 @@ class Sketch:
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass
             self._h = None
+
+    # ------------------------------------------------------------------ profiling
+    def set_profiling(self, enable: bool = True) -> None:
+        _check(self._lib.sketch_set_profiling(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{phase: (device ms summed over launches, launch count)}; clears the record."""
+        ms = (ctypes.c_double * len(PHASES))()
+        cnt = (ctypes.c_int64 * len(PHASES))()
+        _check(self._lib.sketch_profile_read(self._h, ms, cnt))
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(PHASES)}
 
     # ------------------------------------------------------------------ workspace
     def workspace_size(self, n1: int) -> int:
@@ -249,6 +266,11 @@ class Sketch:
         _check(self._lib.sketch_generate_bits(self._h, row0, nrows, col0, ncols, out.data_ptr(),
                                               max(ncols, 1), _stream_ptr(stream)))
         return out
+
+
+def launch_count() -> int:
+    """Kernels launched by libsketch.so in this process so far."""
+    return int(load_library().sketch_launch_count())
 
 
 def debug_box_muller(w1, w2, transform: str = "accurate", stream=None):

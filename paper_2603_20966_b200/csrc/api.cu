@@ -3,13 +3,20 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/sketch.h"
 #include "kernels.cuh"
+
+struct sk_timed_launch {
+    int phase;
+    cudaEvent_t start, end;
+};
 
 struct sk_sketch_s {
     uint64_t seed;
@@ -19,6 +26,34 @@ struct sk_sketch_s {
     int mode;
     int omega_transform;
     int split_override;
+    int profiling;
+    std::mutex prof_mu;
+    std::vector<sk_timed_launch> prof;
+};
+
+static std::atomic<uint64_t> g_launches{0};
+
+// Brackets one kernel launch: counts it and, when profiling, records events on its stream.
+struct LaunchScope {
+    sk_sketch_s* h;
+    int phase;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    LaunchScope(sk_sketch_s* h_, int phase_, cudaStream_t s_) : h(h_), phase(phase_), s(s_) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (h && h->profiling) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, s);
+        }
+    }
+    ~LaunchScope() {
+        if (e0) {
+            cudaEventRecord(e1, s);
+            std::lock_guard<std::mutex> g(h->prof_mu);
+            h->prof.push_back({phase, e0, e1});
+        }
+    }
 };
 
 namespace {
@@ -210,11 +245,15 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
             p.ldo = ldb;
             p.part_stride = 0;
         }
-        cudaError_t e = sk::launch_sketch_gemm(map, p, P.nacc, h->dist, h->mode,
-                                               h->omega_transform == SK_OMEGA_FAST, P.grid,
-                                               P.smem, stream);
+        cudaError_t e;
+        {
+            LaunchScope ls(h, SK_PHASE_SKETCH_GEMM, stream);
+            e = sk::launch_sketch_gemm(map, p, P.nacc, h->dist, h->mode,
+                                       h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
         if (P.split > 1) {
+            LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, stream);
             e = sk::launch_splitk_reduce(static_cast<const float*>(ws), p.part_stride, P.split,
                                          p.n1, p.r_valid, p.npad, B + c0, ldb, stream);
             if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
@@ -243,9 +282,16 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         cudaError_t e = cudaMemset2DAsync(C, ldc * sizeof(float), 0, h->r * sizeof(float), h->r, stream);
         return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "memset C");
     }
-    cudaError_t e = sk::launch_core_gemm(p, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
+    cudaError_t e;
+    {
+        LaunchScope ls(h, SK_PHASE_CORE_GEMM, stream);
+        e = sk::launch_core_gemm(p, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "core_gemm launch");
-    e = sk::launch_core_reduce(p.part, p.chunks, p.r, C, ldc, stream);
+    {
+        LaunchScope ls(h, SK_PHASE_CORE_REDUCE, stream);
+        e = sk::launch_core_reduce(p.part, p.chunks, p.r, C, ldc, stream);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "core_reduce launch");
     return SK_SUCCESS;
 }
@@ -273,17 +319,58 @@ sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, 
     if (r < 1 || r > 4096) return fail(SK_ERR_INVALID_VALUE, "r must be in [1, 4096]");
     if (dist != SK_DIST_GAUSSIAN && dist != SK_DIST_RADEMACHER && dist != SK_DIST_UNIFORM)
         return fail(SK_ERR_INVALID_VALUE, "unknown distribution");
-    auto* h = new (std::nothrow) sk_sketch_s{seed, static_cast<int>(dist), n2, r, sk::kTF32,
-                                             SK_OMEGA_ACCURATE, 0};
+    auto* h = new (std::nothrow) sk_sketch_s;
     if (!h) return fail(SK_ERR_INVALID_VALUE, "out of host memory");
+    h->seed = seed;
+    h->dist = static_cast<int>(dist);
+    h->n2 = n2;
+    h->r = r;
+    h->mode = sk::kTF32;
+    h->omega_transform = SK_OMEGA_ACCURATE;
+    h->split_override = 0;
+    h->profiling = 0;
     *out = h;
     return SK_SUCCESS;
 }
 
 sk_status_t sketch_destroy(sk_sketch_t h) {
-    delete h;
+    if (h) {
+        for (auto& t : h->prof) { cudaEventDestroy(t.start); cudaEventDestroy(t.end); }
+        delete h;
+    }
     return SK_SUCCESS;
 }
+
+sk_status_t sketch_set_profiling(sk_sketch_t h, int enable) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    h->profiling = enable ? 1 : 0;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_profile_read(sk_sketch_t h, double* ms, int64_t* launches) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (!ms || !launches) return fail(SK_ERR_INVALID_VALUE, "NULL output arrays");
+    for (int i = 0; i < SK_PHASE_COUNT; ++i) { ms[i] = 0.0; launches[i] = 0; }
+    std::vector<sk_timed_launch> v;
+    {
+        std::lock_guard<std::mutex> g(h->prof_mu);
+        v.swap(h->prof);
+    }
+    sk_status_t st = SK_SUCCESS;
+    for (auto& t : v) {
+        float e = 0.f;
+        cudaError_t err = cudaEventSynchronize(t.end);
+        if (err == cudaSuccess) err = cudaEventElapsedTime(&e, t.start, t.end);
+        if (err != cudaSuccess && st == SK_SUCCESS) st = cuda_fail(err, "profile event");
+        ms[t.phase] += e;
+        launches[t.phase] += 1;
+        cudaEventDestroy(t.start);
+        cudaEventDestroy(t.end);
+    }
+    return st;
+}
+
+uint64_t sketch_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 sk_status_t sketch_set_mode(sk_sketch_t h, sk_mode_t mode) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
@@ -385,6 +472,7 @@ sk_status_t sketch_generate(sk_sketch_t h, int64_t row0, int64_t nrows, int64_t 
     if (!out || row0 < 0 || nrows < 0 || col0 < 0 || ncols < 0 || col0 + ncols > h->r ||
         row0 + nrows > (1ll << 62) || ld < ncols)
         return fail(SK_ERR_INVALID_VALUE, "block outside [0, 2^62) x [0, r) or bad ld");
+    LaunchScope ls(h, SK_PHASE_GENERATE, static_cast<cudaStream_t>(stream));
     cudaError_t e = sk::launch_generate(h->seed, h->dist, row0, nrows, col0, ncols, out, ld, false,
                                         static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "generate launch");
@@ -396,6 +484,7 @@ sk_status_t sketch_generate_bits(sk_sketch_t h, int64_t row0, int64_t nrows, int
     if (!out || row0 < 0 || nrows < 0 || col0 < 0 || ncols < 0 || col0 + ncols > h->r ||
         row0 + nrows > (1ll << 62) || ld < ncols)
         return fail(SK_ERR_INVALID_VALUE, "block outside [0, 2^62) x [0, r) or bad ld");
+    LaunchScope ls(h, SK_PHASE_GENERATE, static_cast<cudaStream_t>(stream));
     cudaError_t e = sk::launch_generate(h->seed, h->dist, row0, nrows, col0, ncols, out, ld, true,
                                         static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "generate_bits launch");
@@ -406,6 +495,7 @@ sk_status_t sketch_debug_box_muller(const uint32_t* w1, const uint32_t* w2, int6
                                     float* out_odd, void* stream) {
     if (n < 0 || (n > 0 && (!w1 || !w2 || !out_even || !out_odd)))
         return fail(SK_ERR_INVALID_VALUE, "bad debug_box_muller arguments");
+    LaunchScope ls(nullptr, SK_PHASE_GENERATE, static_cast<cudaStream_t>(stream));
     cudaError_t e = sk::launch_debug_box_muller(w1, w2, n, transform == SK_OMEGA_FAST, out_even,
                                                 out_odd, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "debug_box_muller launch");

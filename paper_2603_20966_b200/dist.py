@@ -1,0 +1,149 @@
+"""Multi-GPU layouts of the sketch and the Nystrom core (one process per GPU, torch.distributed/NCCL).
+
+Implements Alg. 1 (RandMatMul) and the No-Redist variant of Alg. 2
+(RandCompNys with Psi = Pi) for processor grids p1 x p2 x 1:
+
+  * rank r <-> grid coordinates (i, j) = (r // p2, r % p2)
+  * rank (i, j) owns A_ij = rows R_i x columns K_j of A
+  * All-Gather of A is a no-op because p3 = 1
+  * GenRandom: every rank regenerates Omega rows K_j itself (inside the kernel)
+  * local product B-bar_i = A_ij Omega_Kj
+  * Reduce-Scatter of B-bar_i over the row group {(i, *)}: rank (i, j) keeps
+    rows piece j of R_i (skipped when p2 = 1: zero communication, Thm. 4.2 / Case 1,
+    PAPER.md:350, 438-440)
+  * Nystrom: C-bar = Omega^T_{rows} B_piece regenerated for the owned B rows
+    then AllReduce of the r x r partials (the GPU variant replaces Reduce-Scatter
+    of C by AllReduce; reading R11: full C on every rank).
+
+Bandwidth accounting: predicted words per rank = (1 - 1/p2) n1 r / p1 for B (Alg. 1 cost,
+PAPER.md:427 with p3 = 1) plus the AllReduce payload r^2 for C; measured = bytes handed to
+the collectives.  Row splits are balanced; column splits are multiples of 128 (so each block's
+Omega rows start on a Philox row-group boundary) except the last.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def balanced_split(n: int, parts: int, align: int = 1) -> list:
+    """Boundaries [b_0=0, ..., b_parts=n]; interior boundaries multiples of `align` when possible."""
+    if align > 1 and n >= parts * align:
+        units = -(-n // align)
+        bnd = [min(n, (units * p // parts) * align) for p in range(parts + 1)]
+    else:
+        bnd = [n * p // parts for p in range(parts + 1)]
+    bnd[-1] = n
+    return bnd
+
+
+@dataclass
+class Layout:
+    p1: int
+    p2: int
+
+    @property
+    def P(self) -> int:
+        return self.p1 * self.p2
+
+    def coords(self, rank: int) -> tuple:
+        return rank // self.p2, rank % self.p2
+
+    @staticmethod
+    def parse(spec: str, P: int) -> "Layout":
+        """'row' -> P x 1, 'col' -> 1 x P, 'AxB' -> A x B (must multiply to P)."""
+        if spec in ("row", "rowblock"):
+            return Layout(P, 1)
+        if spec in ("col", "colblock"):
+            return Layout(1, P)
+        a, b = (int(t) for t in spec.lower().split("x"))
+        if a * b != P:
+            raise ValueError(f"layout {spec} does not match world size {P}")
+        return Layout(a, b)
+
+
+def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool) -> int:
+    """Alg. 1 reduce-scatter volume (1 - 1/p2) n1 r / p1 words (+ r^2 AllReduce payload), fp32."""
+    words = (1.0 - 1.0 / layout.p2) * n1 * r / layout.p1
+    if nystrom and layout.P > 1:
+        words += r * r
+    return int(round(4 * words))
+
+
+class DistSketch:
+    """B = A Omega and (optionally) C = Omega^T B on a p1 x p2 grid of ranks.
+
+    `local` is the per-rank compute: by default the CUDA library (paper_2603_20966_b200.Sketch);
+    tests may inject a CPU stand-in to exercise partitioning and collectives with gloo.
+    """
+
+    def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
+                 mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128):
+        import torch.distributed as tdist
+        self.tdist = tdist
+        self.group = group
+        self.rank = tdist.get_rank(group)
+        self.world = tdist.get_world_size(group)
+        if layout.P != self.world:
+            raise ValueError("layout size != world size")
+        self.layout = layout
+        self.n1, self.n2, self.r = n1, n2, r
+        self.i, self.j = layout.coords(self.rank)
+        self.row_bnd = balanced_split(n1, layout.p1)
+        self.col_bnd = balanced_split(n2, layout.p2, col_align)
+        if local is None:
+            from . import Sketch
+            local = Sketch(seed, dist, n2, r, mode=mode, omega=omega)
+        self.local = local
+        # row group {(i, *)} for the reduce-scatter of B
+        self.row_group = group
+        if layout.p2 > 1 and layout.p1 > 1:
+            groups = [tdist.new_group([ii * layout.p2 + jj for jj in range(layout.p2)])
+                      for ii in range(layout.p1)]
+            self.row_group = groups[self.i]
+        elif layout.p2 > 1:
+            self.row_group = group
+        self.comm_bytes = 0
+
+    # ------------------------------------------------------------------ partition
+    def a_block_range(self) -> tuple:
+        """(row0, row1, col0, col1) of A_ij owned by this rank."""
+        return (self.row_bnd[self.i], self.row_bnd[self.i + 1],
+                self.col_bnd[self.j], self.col_bnd[self.j + 1])
+
+    def b_piece_rows(self) -> tuple:
+        """Global rows of B this rank owns after the reduce-scatter: piece j of R_i."""
+        r0, r1 = self.row_bnd[self.i], self.row_bnd[self.i + 1]
+        if self.layout.p2 == 1:
+            return r0, r1
+        per = -(-(r1 - r0) // self.layout.p2)
+        a = min(r1, r0 + self.j * per)
+        return a, min(r1, a + per)
+
+    # ------------------------------------------------------------------ Alg. 1
+    def apply(self, A_blk):
+        """Returns (B_piece, (row0, row1)): the rows of B = A Omega this rank owns."""
+        import torch
+        r0, r1, c0, c1 = self.a_block_range()
+        assert tuple(A_blk.shape) == (r1 - r0, c1 - c0), (A_blk.shape, (r1 - r0, c1 - c0))
+        p2 = self.layout.p2
+        if p2 == 1:
+            return self.local.apply_block(A_blk, c0), (r0, r1)
+        rows = r1 - r0
+        per = -(-rows // p2)
+        Bbar = torch.zeros((per * p2, self.r), dtype=torch.float32, device=A_blk.device)
+        self.local.apply_block(A_blk, c0, out=Bbar[:rows])
+        piece = torch.empty((per, self.r), dtype=torch.float32, device=A_blk.device)
+        self.tdist.reduce_scatter_tensor(piece, Bbar, group=self.row_group)
+        self.comm_bytes += Bbar.numel() * 4 * (p2 - 1) // p2
+        a, b = self.b_piece_rows()
+        return piece[: b - a], (a, b)
+
+    # ------------------------------------------------------------------ Alg. 2 (No-Redist)
+    def nystrom_core(self, A_blk):
+        """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank."""
+        Bp, (a, b) = self.apply(A_blk)
+        C = self.local.core_block(Bp, a)
+        if self.world > 1:
+            self.tdist.all_reduce(C, group=self.group)
+            self.comm_bytes += C.numel() * 4
+        return Bp, (a, b), C

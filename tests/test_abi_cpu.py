@@ -13,7 +13,7 @@ from tests.conftest import ROOT
 def _declared_functions():
     src = open(os.path.join(ROOT, "include", "sketch.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:sk_status_t|const char\*)\s+(\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:sk_status_t|const char\*|uint64_t)\s+(\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_declares_expected_entry_points():
