@@ -87,6 +87,15 @@ sk_status_t sketch_set_omega_transform(sk_sketch_t h, sk_omega_transform_t t);
 /* Tuning override for the split-K factor of the sketch GEMM (0 = automatic, else 1..64). */
 sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k);
 
+/* Tuning / ablation override of the sketch GEMM's CTA grouping: 0 = automatic (CTA pairs with
+ * tcgen05 cta_group::2 for n1 > 256), 1 = single-CTA tiles, 2 = CTA pairs when n1 > 256. */
+sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg);
+
+/* Performance ablation for measurements only (results are WRONG while set): bit 0 skips the
+ * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs.  0 restores
+ * normal operation. */
+sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags);
+
 /* Bytes of device workspace needed by sketch_apply / sketch_apply_block on n1 rows and
  * nystrom_core / core_apply_block (split-K partials of B and per-CTA r x r partials of C).
  * One size covers every entry point for that n1 (n for nystrom_core). */

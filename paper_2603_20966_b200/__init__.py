@@ -24,7 +24,8 @@ _OMEGA = {"accurate": 0, "fast": 1}
 
 EXPORTED_SYMBOLS = (
     "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
-    "sketch_set_split_k", "sketch_workspace_size", "sketch_apply", "nystrom_core",
+    "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_ablation",
+    "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "sketch_generate", "sketch_generate_bits",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
@@ -67,6 +68,8 @@ def load_library(build_if_missing: bool = True):
         lib.sketch_set_mode.argtypes = [vp, ctypes.c_int]
         lib.sketch_set_omega_transform.argtypes = [vp, ctypes.c_int]
         lib.sketch_set_split_k.argtypes = [vp, i32]
+        lib.sketch_set_cta_group.argtypes = [vp, i32]
+        lib.sketch_set_ablation.argtypes = [vp, ctypes.c_uint32]
         lib.sketch_workspace_size.argtypes = [vp, i64, ctypes.POINTER(sz)]
         lib.sketch_apply.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, sz, vp]
         lib.nystrom_core.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
@@ -141,7 +144,7 @@ class Sketch:
     """
 
     def __init__(self, seed: int, dist, n2: int, r: int, mode: str = "tf32",
-                 omega: str = "accurate", split_k: int = 0):
+                 omega: str = "accurate", split_k: int = 0, cta_group: int = 0):
         self._lib = load_library()
         self.seed, self.n2, self.r = int(seed), int(n2), int(r)
         self.dist = _DISTS[dist] if isinstance(dist, str) else int(dist)
@@ -152,6 +155,7 @@ class Sketch:
         _check(self._lib.sketch_set_mode(h, MODES[mode]))
         _check(self._lib.sketch_set_omega_transform(h, _OMEGA[omega]))
         _check(self._lib.sketch_set_split_k(h, int(split_k)))
+        _check(self._lib.sketch_set_cta_group(h, int(cta_group)))
         self._ws = {}
 
     def __del__(self):
@@ -162,6 +166,10 @@ class Sketch:
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass
             self._h = None
+
+    def set_ablation(self, flags: int) -> None:
+        """Measurement-only switches (bit 0: no Omega generation, bit 1: no A loads); results wrong."""
+        _check(self._lib.sketch_set_ablation(self._h, int(flags)))
 
     # ------------------------------------------------------------------ profiling
     def set_profiling(self, enable: bool = True) -> None:

@@ -26,6 +26,8 @@ struct sk_sketch_s {
     int mode;
     int omega_transform;
     int split_override;
+    int cg_override;  // 0 auto, 1 force single-CTA tiles (ablation / tests)
+    uint32_t ablate;  // performance ablations (bench only): see SketchGemmParams::ablate
     int profiling;
     std::mutex prof_mu;
     std::vector<sk_timed_launch> prof;
@@ -108,6 +110,7 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 struct SketchPlan {
     int npass;         // column passes of <= 256 columns
     int npad[32];      // MMA N per pass
+    int cg;            // 1: one CTA per tile; 2: CTA pair (tcgen05 cta_group::2, M = 256)
     int nacc;
     int a_stages, o_stages;
     int split;
@@ -127,16 +130,20 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
         P.npad[i] = static_cast<int>(std::min<int64_t>(256, rpad - 256 * i));
         npad_max = std::max(npad_max, P.npad[i]);
     }
-    P.nacc = (n1 > 128) ? 2 : 1;
-    P.o_stages = 2;
+    P.cg = (n1 > 256 && h->cg_override != 1) ? 2 : 1;
+    P.nacc = (n1 > 128 * P.cg) ? 2 : 1;
+    // CTA pairs hand every Omega stage across the pair (relay + multicast commit): a deeper ring
+    // hides that round trip.
+    P.o_stages = (P.cg == 2) ? 4 : 2;
     const int budget = sk::sketch_gemm_max_smem() - 2048;
     const int a_stage = P.nacc * 128 * 32 * 4;
-    P.a_stages = std::min(6, (budget - P.o_stages * npad_max * 128) / a_stage);
-    P.smem = sk::sketch_gemm_smem_bytes(P.nacc, npad_max, P.a_stages, P.o_stages);
+    P.a_stages = std::min(6, (budget - P.o_stages * (npad_max / P.cg) * 128) / a_stage);
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages);
     P.kiters = static_cast<int>((k + kshift + 31) / 32);
-    P.num_mblk = static_cast<int>((n1 + 128 * P.nacc - 1) / (128 * P.nacc));
+    const int rows_per_unit = 128 * P.cg * P.nacc;
+    P.num_mblk = static_cast<int>((n1 + rows_per_unit - 1) / rows_per_unit);
     P.ws_per_split = static_cast<size_t>(n1) * npad_max * sizeof(float);
-    const int nsm = sk::num_sms();
+    const int nsm = sk::num_sms() / P.cg;  // independent workers (CTAs or CTA pairs)
     int best_s = 1;
     if (h->split_override > 0) {
         best_s = std::min(h->split_override, std::max(1, P.kiters));
@@ -150,7 +157,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
             double t = static_cast<double>(waves) * (kper + unit_ovh);
             if (s > 1)
                 t += static_cast<double>(s + 1) * n1 * npad_max * 4.0 /
-                     (static_cast<double>(nsm) * a_stage);
+                     (static_cast<double>(nsm) * a_stage * P.cg);
             if (t < best * 0.995) { best = t; best_s = s; }
         }
     }
@@ -160,7 +167,8 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int kper = (P.kiters + best_s - 1) / best_s;
     P.split = (P.kiters + kper - 1) / kper;
     const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
-    P.grid = static_cast<int>(std::min<int64_t>(units, nsm));
+    P.grid = static_cast<int>(std::min<int64_t>(units, nsm)) * P.cg;
+    if ((h->ablate & 8u) && (P.grid & 1)) P.grid += 1;  // cluster-of-2 ablation needs an even grid
     return P;
 }
 
@@ -236,6 +244,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.o_stages = P.o_stages;
         p.key0 = static_cast<uint32_t>(h->seed);
         p.key1 = static_cast<uint32_t>(h->seed >> 32);
+        p.ablate = h->ablate;
         if (P.split > 1) {
             p.out = static_cast<float*>(ws);
             p.ldo = p.npad;
@@ -248,7 +257,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         cudaError_t e;
         {
             LaunchScope ls(h, SK_PHASE_SKETCH_GEMM, stream);
-            e = sk::launch_sketch_gemm(map, p, P.nacc, h->dist, h->mode,
+            e = sk::launch_sketch_gemm(map, p, P.cg, P.nacc, h->dist, h->mode,
                                        h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
@@ -328,6 +337,8 @@ sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, 
     h->mode = sk::kTF32;
     h->omega_transform = SK_OMEGA_ACCURATE;
     h->split_override = 0;
+    h->cg_override = 0;
+    h->ablate = 0;
     h->profiling = 0;
     *out = h;
     return SK_SUCCESS;
@@ -392,6 +403,19 @@ sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
     if (split_k < 0 || split_k > 64) return fail(SK_ERR_INVALID_VALUE, "split_k must be in [0, 64]");
     h->split_override = split_k;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (cg < 0 || cg > 2) return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1 or 2");
+    h->cg_override = cg;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    h->ablate = flags & 31u;
     return SK_SUCCESS;
 }
 

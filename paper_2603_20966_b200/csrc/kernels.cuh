@@ -30,6 +30,7 @@ struct SketchGemmParams {
     int32_t a_stages;     // A smem pipeline depth
     int32_t o_stages;     // Omega smem pipeline depth
     uint32_t key0, key1;  // Philox key = (seed lo, seed hi)
+    uint32_t ablate;      // 0 in production; bit 0: skip Omega generation, bit 1: skip A loads
 };
 
 struct CoreGemmParams {
@@ -55,10 +56,10 @@ struct LaunchCfg {
 };
 
 // Host-side launchers (return cudaError_t of the launch).
-cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int nacc,
-                               int dist, int mode, bool fast, int grid, size_t smem,
+cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg,
+                               int nacc, int dist, int mode, bool fast, int grid, size_t smem,
                                cudaStream_t s);
-size_t sketch_gemm_smem_bytes(int nacc, int npad, int a_stages, int o_stages);
+size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages);
 int sketch_gemm_max_smem();
 
 cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,

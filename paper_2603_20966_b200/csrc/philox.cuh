@@ -50,16 +50,65 @@ __device__ __forceinline__ uint4 philox_rade_call(uint64_t g, uint32_t col, uint
 }
 
 // ---------------------------------------------------------------------------------------------
-// Box-Muller, accurate fp32: logf (<=1 ulp), correctly rounded sqrtf, sincospif with exact
-// argument reduction (2 u2 is exact), one rounding per product.  Exact zeros at u2 in
-// {0, 1/4, 1/2, 3/4} and R = 0 at u1 = 1 (reading R14).
+// Box-Muller, accurate fp32 (<= 2 ulp against the correctly rounded value, checked exhaustively
+// over every u1 and every u2 by tests/test_gpu_parity.py).  Exact zeros at u2 in {0, 1/4, 1/2,
+// 3/4} and R = 0 at u1 = 1 (reading R14).
+// -ln(u1) for u1 = M 2^-24, M in [1, 2^24] (exact fp32).  Reduction u1 = 2^k f, f in
+// [sqrt(2)/2, sqrt(2)) by integer ops on the bit pattern; ln f = log1p(t), t = f - 1 (exact), via
+// s = t / (2 + t) and the minimax series of FreeBSD's e_logf.c (< 1 ulp); the reciprocal is the
+// approximate MUFU.RCP, whose 2^-22 error only reaches the small correction term s*(hfsq + R).
+__device__ __forceinline__ float neg_log_u1(float u1) {
+    const uint32_t ix = __float_as_uint(u1) - 0x3F3504F3u;
+    const int k = static_cast<int>(ix) >> 23;                      // exponent after reduction
+    const float f = __uint_as_float((ix & 0x007FFFFFu) + 0x3F3504F3u) - 1.0f;
+    float r2;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(2.0f + f));
+    const float s = f * r2;
+    const float z = s * s;
+    const float w = z * z;
+    const float t1 = w * fmaf(w, 0xf89e26.0p-26f, 0xccce13.0p-25f);
+    const float t2 = z * fmaf(w, 0x91e9ee.0p-25f, 0xaaaaaa.0p-24f);
+    const float R = t2 + t1;
+    const float hfsq = 0.5f * f * f;
+    const float dk = static_cast<float>(k);
+    // ln u1 = k ln2_hi + (f - hfsq + s (hfsq + R) + k ln2_lo)
+    const float lnf = fmaf(s, hfsq + R, fmaf(dk, 9.0580006145e-06f, -hfsq)) + f;
+    return -fmaf(dk, 6.9313812256e-01f, lnf);
+}
+
+// (cos 2 pi u2, sin 2 pi u2) for u2 = a 2^-24: exact quadrant reduction in integers
+// (a = q 2^22 + rem, rem in [-2^21, 2^21)), y = rem / 2^22 in [-1/2, 1/2] (exact), then
+// sin(pi y / 2) and cos(pi y / 2) by their Taylor series to y^9 / y^10 (truncation < 2^-28) with
+// the leading sine coefficient split hi + lo, and finally the rotation by q quarter turns.
+__device__ __forceinline__ float2 cos_sin_2pi(uint32_t a) {
+    const uint32_t qa = (a + (1u << 21)) >> 22;
+    const uint32_t q = qa & 3u;
+    const int32_t rem = static_cast<int32_t>(a) - static_cast<int32_t>(qa << 22);
+    const float y = __int2float_rn(rem) * 0x1p-22f;
+    const float y2 = y * y;
+    float sp = fmaf(y2, 1.60441185e-04f, -4.68175413e-03f);
+    sp = fmaf(y2, sp, 7.96926262e-02f);
+    sp = fmaf(y2, sp, -6.45964098e-01f);
+    const float sn = fmaf(y, 1.57079637e+00f, fmaf(y, -4.37113883e-08f, (y * y2) * sp));
+    float cp = fmaf(y2, -2.52020424e-05f, 9.19260275e-04f);
+    cp = fmaf(y2, cp, -2.08634808e-02f);
+    cp = fmaf(y2, cp, 2.53669508e-01f);
+    cp = fmaf(y2, cp, -1.23370055e+00f);
+    const float cs = fmaf(y2, cp, 1.0f);
+    // rotate by q quarter turns: (c, s) -> (c,s), (-s,c), (-c,-s), (s,-c)
+    const float c0 = (q & 1u) ? sn : cs;
+    const float s0 = (q & 1u) ? cs : sn;
+    const uint32_t negc = ((q + 1u) & 2u) << 30;  // q = 1, 2
+    const uint32_t negs = (q & 2u) << 30;         // q = 2, 3
+    return make_float2(__uint_as_float(__float_as_uint(c0) ^ negc),
+                       __uint_as_float(__float_as_uint(s0) ^ negs));
+}
+
 __device__ __forceinline__ float2 box_muller_accurate(uint32_t w1, uint32_t w2) {
     const float u1 = __uint2float_rn((w1 >> 8) + 1u) * 0x1p-24f;  // (0,1], exact
-    const float t = __uint2float_rn(w2 >> 8) * 0x1p-23f;          // 2 u2 in [0,2), exact
-    const float R = sqrtf(-2.0f * logf(u1));
-    float s, c;
-    sincospif(t, &s, &c);
-    return make_float2(R * c, R * s);
+    const float R = sqrtf(2.0f * neg_log_u1(u1));
+    const float2 cs = cos_sin_2pi(w2 >> 8);
+    return make_float2(R * cs.x, R * cs.y);
 }
 
 // Box-Muller on the MUFU special-function unit (lg2 / sqrt / sin / cos .approx); allowed only

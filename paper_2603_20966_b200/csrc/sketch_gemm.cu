@@ -2,17 +2,22 @@
 // the local product of Alg. 1 ("B-bar_ik = A_ij * Omega_jk") with Omega_jk
 // regenerated in the kernel instead of communicated.
 //
-// One persistent CTA per SM, warp-specialised:
+// One persistent CTA per SM (CG = 1) or per SM of a CTA pair (CG = 2, cluster (2,1,1),
+// tcgen05 cta_group::2: the pair computes M = 256 rows per accumulator; each CTA holds its own
+// 128 rows of A and HALF of the Omega tile's N columns, so each CTA generates only npad/2 Omega
+// columns -- the pair shares every generated Omega element across 256 rows of A).  Warps:
 //   warp 0      TMA producer: 128-row x 32-col fp32 tiles of A, SWIZZLE_128B (K-major), into an
-//               a_stages-deep ring; L2 evict-first (A is streamed exactly once).
-//   warp 1      MMA issuer (one elected thread): tcgen05.mma kind::tf32, M=128, N=npad, K=8,
-//               NACC accumulators of 128 x npad fp32 in TMEM (NACC*npad <= 512 columns).
+//               a_stages-deep ring; L2 evict-first (A is streamed exactly once).  With CG = 2
+//               both CTAs load their rows and the bytes are counted on the leader's barrier.
+//   warp 1      MMA issuer (one elected thread of the leader CTA): tcgen05.mma kind::tf32,
+//               M = 128*CG, N = npad, K = 8; NACC accumulators of 128 x npad fp32 per CTA in TMEM.
 //   warp 2      TMEM allocator.
-//   warps 4-11  Omega producers: Philox4x32-10 + transform, written as the K-major SWIZZLE_128B
-//               B operand (row n = Omega column c0+n, 32 K-values = 128 B per row), then
-//               fence.proxy.async + mbarrier arrive.  Warps 4-7 also run the epilogue
-//               (tcgen05.ld 32x32b -> st.global of B or of a split-K partial).
-// Work unit = (m-block of 128*NACC rows, K split s); units are dealt round-robin to CTAs.
+//   warps 4-19  Omega producers: Philox4x32-10 + transform, written as the K-major SWIZZLE_128B
+//               B operand (row n = Omega column, 32 K-values = 128 B per row), then
+//               fence.proxy.async + one mbarrier arrive per warp (remote on the leader for CG = 2).
+//               Warps 4-7 also run the epilogue (tcgen05.ld 32x32b -> st.global of B or of a
+//               split-K partial).
+// Work unit = (m-block of 128*CG*NACC rows, K split s); units are dealt round-robin to CTA groups.
 #include "kernels.cuh"
 #include "philox.cuh"
 #include "ptx.cuh"
@@ -20,7 +25,7 @@
 namespace sk {
 
 constexpr int kCtlWarps = 4;
-constexpr int kRngWarps = 8;
+constexpr int kRngWarps = 16;
 constexpr int kThreads = (kCtlWarps + kRngWarps) * 32;
 constexpr int kRngThreads = kRngWarps * 32;
 constexpr uint32_t kATileBytes = 128 * 32 * 4;  // one 128-row x 32-fp32 TMA box
@@ -68,16 +73,17 @@ __device__ __forceinline__ uint32_t pick_word(uint4 x, uint32_t sel) {
     return sel == 0 ? x.x : sel == 1 ? x.y : sel == 2 ? x.z : x.w;
 }
 
+// Rademacher tile: one Philox call per column n = t serves all 32 K-values of the tile.
 template <int DIST, int MODE, bool FAST>
-__device__ __forceinline__ void produce_omega_tile(uint8_t* tile, int64_t kglob0, int roff,
-                                                   int npad, int c0, uint32_t key0,
-                                                   uint32_t key1, int t) {
+__device__ __forceinline__ void produce_omega_tile_r(uint8_t* tile, int64_t kglob0, int roff,
+                                                     int npad, int c0, uint32_t key0,
+                                                     uint32_t key1, int t) {
     if (t >= npad) return;
     const int n = t;
     const uint32_t col = static_cast<uint32_t>(c0 + n);
     const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
     const uint32_t sw = static_cast<uint32_t>(n & 7);
-    if constexpr (DIST == kRademacher) {
+    {
         // bits for tile rows kk = 0..31: global rows kglob0 + kk
         const uint64_t g = static_cast<uint64_t>(kglob0);
         const uint4 x = philox_rade_call(g >> 7, col, key0, key1);
@@ -94,41 +100,72 @@ __device__ __forceinline__ void produce_omega_tile(uint8_t* tile, int64_t kglob0
                                          rade_from_bit(w, 4 * j4 + 2), rade_from_bit(w, 4 * j4 + 3));
             store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v);
         }
-    } else {
-        const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;
-        if (roff == 0) {
-#pragma unroll 2
-            for (int j4 = 0; j4 < 8; ++j4) {
-                const float4 v = values4<DIST, FAST>(philox_gauss_call(q0 + j4, col, key0, key1));
-                store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v);
-            }
-        } else {
-            // chunk j4 = rows 4(q0+j4)+roff .. +3: last 4-roff values of call q0+j4, first roff of
-            // call q0+j4+1
-            float4 prev = values4<DIST, FAST>(philox_gauss_call(q0, col, key0, key1));
-#pragma unroll 1
-            for (int j4 = 0; j4 < 8; ++j4) {
-                const float4 next = values4<DIST, FAST>(philox_gauss_call(q0 + j4 + 1, col, key0, key1));
-                const float a[8] = {prev.x, prev.y, prev.z, prev.w, next.x, next.y, next.z, next.w};
-                float4 v;
-                v.x = roff == 1 ? a[1] : roff == 2 ? a[2] : a[3];
-                v.y = roff == 1 ? a[2] : roff == 2 ? a[3] : a[4];
-                v.z = roff == 1 ? a[3] : roff == 2 ? a[4] : a[5];
-                v.w = roff == 1 ? a[4] : roff == 2 ? a[5] : a[6];
-                store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v);
-                prev = next;
-            }
-        }
     }
 }
 
-template <int NACC, int DIST, int MODE, bool FAST>
+// Gaussian / uniform tile: the npad x 8 chunks (one Philox call -> 4 K-values each) are dealt to
+// the kRngThreads producers as c = t + kRngThreads * i, n = c % npad, j4 = c / npad, so a warp
+// stores 32 consecutive rows n at one j4 (conflict-free under the 128-B swizzle).
+template <int DIST, int MODE, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglob0, int roff,
+                                                     int npad, int c0, uint32_t key0,
+                                                     uint32_t key1, int n_start, int j_start,
+                                                     int tq, int tr) {
+    const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;
+    const uint32_t tile_base = smem_u32(tile);
+    int n = n_start, j4 = j_start;
+    if (roff == 0) {
+        // two independent chunks per iteration: their Philox / Box-Muller chains interleave
+#pragma unroll 1
+        while (j4 < 8) {
+            int n2 = n + tr, j2 = j4 + tq;
+            if (n2 >= npad) { n2 -= npad; ++j2; }
+            const bool two = j2 < 8;
+            const int n2c = two ? n2 : n, j2c = two ? j2 : j4;
+            const uint4 xa = philox_gauss_call(q0 + j4, static_cast<uint32_t>(c0 + n), key0, key1);
+            const uint4 xb = philox_gauss_call(q0 + j2c, static_cast<uint32_t>(c0 + n2c), key0, key1);
+            const float4 va = values4<DIST, FAST>(xa);
+            const float4 vb = values4<DIST, FAST>(xb);
+            store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n) * 128u +
+                                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4), va);
+            if (two)
+                store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n2) * 128u +
+                                                  ((static_cast<uint32_t>(j2) ^ static_cast<uint32_t>(n2 & 7)) << 4), vb);
+            n = n2 + tr;
+            j4 = j2 + tq;
+            if (n >= npad) { n -= npad; ++j4; }
+        }
+        return;
+    }
+#pragma unroll 1
+    for (; j4 < 8;) {
+        const uint32_t col = static_cast<uint32_t>(c0 + n);
+        const uint32_t addr = tile_base + static_cast<uint32_t>(n) * 128u +
+                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4);
+        // rows 4(q0+j4)+roff .. +3: tail of call q0+j4, head of call q0+j4+1
+        const float4 a0 = values4<DIST, FAST>(philox_gauss_call(q0 + j4, col, key0, key1));
+        const float4 a1 = values4<DIST, FAST>(philox_gauss_call(q0 + j4 + 1, col, key0, key1));
+        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        float4 v;
+        v.x = roff == 1 ? a[1] : roff == 2 ? a[2] : a[3];
+        v.y = roff == 1 ? a[2] : roff == 2 ? a[3] : a[4];
+        v.z = roff == 1 ? a[3] : roff == 2 ? a[4] : a[5];
+        v.w = roff == 1 ? a[4] : roff == 2 ? a[5] : a[6];
+        store_chunk<DIST, MODE, FAST>(addr, v);
+        n += tr;
+        j4 += tq;
+        if (n >= npad) { n -= npad; ++j4; }
+    }
+}
+
+template <int CG, int NACC, int DIST, int MODE, bool FAST>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    const SmemLayout L = make_layout(NACC, p.npad, p.a_stages, p.o_stages);
+    const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
+    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages);
     uint8_t* sA = smem + L.a_off;
     uint8_t* sO = smem + L.o_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -142,52 +179,85 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;
+    const bool leader = crank == 0;
+    const int group = static_cast<int>(blockIdx.x) / CG;
+    const int ngroups = static_cast<int>(gridDim.x) / CG;
     uint32_t tmem_cols = 32;
     while (tmem_cols < static_cast<uint32_t>(NACC * p.npad)) tmem_cols <<= 1;
 
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < p.a_stages; ++s) { mbar_init(&full_a[s], 1); mbar_init(&empty_a[s], 1); }
+        // full_a: one expect_tx arrival; with CG = 2 the leader's barrier counts the bytes of BOTH
+        // CTAs' TMA loads (the peer's loads complete_tx on it directly)
+        for (int s = 0; s < p.a_stages; ++s) {
+            mbar_init(&full_a[s], 1);
+            mbar_init(&empty_a[s], 1);
+        }
         for (int s = 0; s < p.o_stages; ++s) {
-            mbar_init(&full_o[s], kRngThreads);
+            // leader: its own kRngWarps warps + (CG = 2) one relayed arrival for the peer's half;
+            // peer: its own kRngWarps warps (forwarded by the relay thread, warp 3)
+            mbar_init(&full_o[s], kRngWarps + ((CG == 2 && leader) ? 1 : 0));
             mbar_init(&empty_o[s], 1);
         }
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 128);
+        mbar_init(tmem_empty, 4 * CG);
         fence_barrier_init();
         tma_prefetch_desc(&tmA);
     }
-    if (warp == 2) tmem_alloc_rt(tmem_slot, tmem_cols);
+    if (warp == 2) {
+        if constexpr (CG == 2) tmem_alloc_pair(tmem_slot, tmem_cols);
+        else tmem_alloc_rt(tmem_slot, tmem_cols);
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total_units = p.num_mblk * p.split;
+    const int rows_per_unit = 128 * CG * NACC;
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint64_t pol = l2_policy_evict_first();
+            const uint32_t a_bytes_cta = L.a_stage;
             uint32_t st = 0, ph = 0;
-            for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+            for (int u = group; u < total_units; u += ngroups) {
                 const int mb = u / p.split, s = u - (u / p.split) * p.split;
                 const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
                 for (int kit = kb; kit < ke; ++kit) {
                     mbar_wait(&empty_a[st], ph ^ 1);
-                    mbar_arrive_expect_tx(&full_a[st], L.a_stage);
+                    const int x = kit * 32 - p.kshift;
+                    if (p.ablate & 2u) {  // ablation: no A traffic, stage marked full at once
+                        if (leader) mbar_arrive(&full_a[st]);
+                        if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
+                        continue;
+                    }
+                    if constexpr (CG == 2) {
+                        // both CTAs load their own rows; bytes are counted on the leader's barrier
+                        const uint32_t bar = mapa_shared(smem_u32(&full_a[st]), 0);
+                        if (leader) mbar_arrive_expect_tx(&full_a[st], 2 * a_bytes_cta);
 #pragma unroll
-                    for (int a = 0; a < NACC; ++a)
-                        tma_load_2d(sA + st * L.a_stage + a * kATileBytes, &tmA, &full_a[st],
-                                    kit * 32 - p.kshift, (mb * NACC + a) * 128, pol);
+                        for (int a = 0; a < NACC; ++a)
+                            tma_load_2d_pair(sA + st * L.a_stage + a * kATileBytes, &tmA, bar, x,
+                                             mb * rows_per_unit + a * 256 + static_cast<int>(crank) * 128, pol);
+                    } else {
+                        mbar_arrive_expect_tx(&full_a[st], a_bytes_cta);
+#pragma unroll
+                        for (int a = 0; a < NACC; ++a)
+                            tma_load_2d(sA + st * L.a_stage + a * kATileBytes, &tmA, &full_a[st], x,
+                                        mb * rows_per_unit + a * 128, pol);
+                    }
                     if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------------ MMA issuer
-        if (elect_one()) {
-            const uint32_t idesc = make_idesc(kFmtTF32, 128, static_cast<uint32_t>(p.npad), 0, 0);
+        // ------------------------------------------------------------------ MMA issuer (leader)
+        if (leader && elect_one()) {
+            const uint32_t idesc = make_idesc(kFmtTF32, 128 * CG, static_cast<uint32_t>(p.npad), 0, 0);
             uint32_t sa = 0, pa = 0, so = 0, po = 0, local = 0;
-            for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++local) {
+            for (int u = group; u < total_units; u += ngroups, ++local) {
                 const int s = u - (u / p.split) * p.split;
                 const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
                 mbar_wait(tmem_empty, (local & 1) ^ 1);
@@ -199,51 +269,90 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a_base = smem_u32(sA + sa * L.a_stage);
                     const uint32_t o_base = smem_u32(sO + so * L.o_stage);
 #pragma unroll
-                    for (int k8 = 0; k8 < 4; ++k8) {
+                    for (int k8 = 0; k8 < ((p.ablate & 4u) ? 0 : 4); ++k8) {
                         const uint64_t bdesc = sw128_desc(o_base + k8 * 32, 16, 1024);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a) {
                             const uint64_t adesc = sw128_desc(a_base + a * kATileBytes + k8 * 32, 16, 1024);
-                            mma_tf32(tmem_base + a * p.npad, adesc, bdesc, idesc,
-                                     (kit > kb || k8 > 0) ? 1u : 0u);
+                            const uint32_t acc = (kit > kb || k8 > 0) ? 1u : 0u;
+                            if constexpr (CG == 2) mma_tf32_pair(tmem_base + a * p.npad, adesc, bdesc, idesc, acc);
+                            else mma_tf32(tmem_base + a * p.npad, adesc, bdesc, idesc, acc);
                         }
                     }
-                    mma_commit(&empty_a[sa]);
-                    mma_commit(&empty_o[so]);
+                    if constexpr (CG == 2) {
+                        mma_commit_pair(&empty_a[sa], 0x3);
+                        mma_commit_pair(&empty_o[so], 0x3);
+                    } else {
+                        mma_commit(&empty_a[sa]);
+                        mma_commit(&empty_o[so]);
+                    }
                     if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                     if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
                 }
-                mma_commit(tmem_full);
+                if constexpr (CG == 2) mma_commit_pair(tmem_full, 0x3);
+                else mma_commit(tmem_full);
+            }
+        }
+    } else if (warp == 2 || warp == 3) {
+        // ------------------------------------------------------------------ relays (peer CTA)
+        // The peer's producer warps arrive on its LOCAL full_o (cheap, CTA scope); one thread
+        // (warp 2) forwards a single release.cluster arrive per stage to the leader's full_o,
+        // keeping the cluster-scope fence off the producers' critical path.
+        if (CG == 2 && !leader && warp == 2 && elect_one()) {
+            uint64_t* bars_r = full_o;
+            const uint32_t nst = static_cast<uint32_t>(p.o_stages);
+            uint32_t st = 0, ph = 0;
+            for (int u = group; u < total_units; u += ngroups) {
+                const int s = u - (u / p.split) * p.split;
+                const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+                for (int kit = kb; kit < ke; ++kit) {
+                    mbar_wait(&bars_r[st], ph);
+                    if (p.ablate & 16u) mbar_arrive_cluster(mapa_shared(smem_u32(&bars_r[st]), 0));
+                    else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&bars_r[st]), 0));
+                    if (++st == nst) { st = 0; ph ^= 1; }
+                }
             }
         }
     } else if (warp >= kCtlWarps) {
         // ------------------------------------------------------------------ Omega producers + epilogue
         const int t = static_cast<int>(threadIdx.x) - kCtlWarps * 32;
+        const int n_start = t % npad_loc, j_start = t / npad_loc;
+        const int tq = kRngThreads / npad_loc, tr = kRngThreads % npad_loc;
+        const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc;
         uint32_t so = 0, po = 0, local = 0;
-        for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++local) {
+        for (int u = group; u < total_units; u += ngroups, ++local) {
             const int mb = u / p.split, s = u - (u / p.split) * p.split;
             const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
             for (int kit = kb; kit < ke; ++kit) {
                 mbar_wait(&empty_o[so], po ^ 1);
-                produce_omega_tile<DIST, MODE, FAST>(sO + so * L.o_stage,
-                                                     p.k0a + static_cast<int64_t>(kit) * 32,
-                                                     p.roff, p.npad, p.c0, p.key0, p.key1, t);
+                if (p.ablate & 1u) {
+                    // ablation: stage marked full without generating Omega
+                } else if constexpr (DIST == kRademacher)
+                    produce_omega_tile_r<DIST, MODE, FAST>(sO + so * L.o_stage,
+                                                           p.k0a + static_cast<int64_t>(kit) * 32,
+                                                           p.roff, npad_loc, c0_loc, p.key0, p.key1, t);
+                else
+                    produce_omega_tile_g<DIST, MODE, FAST>(sO + so * L.o_stage,
+                                                           p.k0a + static_cast<int64_t>(kit) * 32,
+                                                           p.roff, npad_loc, c0_loc, p.key0, p.key1,
+                                                           n_start, j_start, tq, tr);
                 fence_proxy_async_smem();
-                mbar_arrive(&full_o[so]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full_o[so]);
                 if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
             }
             if (t < 128) {
-                // epilogue: warp (4+q) reads TMEM lanes 32q..32q+31
+                // epilogue: warp (4+q) reads TMEM lanes 32q..32q+31 = rows of this CTA's half
                 const int q = t >> 5;
                 mbar_wait(tmem_full, local & 1);
                 tc_fence_after();
                 float* out = p.out + (p.split > 1 ? static_cast<int64_t>(s) * p.part_stride : 0);
+                const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
                 for (int a = 0; a < NACC; ++a) {
-                    const int row = (mb * NACC + a) * 128 + q * 32 + static_cast<int>(lane);
+                    const int row = mb * rows_per_unit + a * 128 * CG + static_cast<int>(crank) * 128 +
+                                    q * 32 + static_cast<int>(lane);
                     float* orow = out + static_cast<int64_t>(row) * p.ldo;
-                    const bool vec_ok = ((p.ldo & 3) == 0) &&
-                                        ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
                     for (int cc = 0; cc < p.npad; cc += 32) {
                         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -274,58 +383,78 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(tmem_empty);
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(tmem_empty), 0));
+                    else mbar_arrive(tmem_empty);
+                }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc_rt(tmem_base, tmem_cols);
+        if constexpr (CG == 2) tmem_dealloc_pair(tmem_base, tmem_cols);
+        else tmem_dealloc_rt(tmem_base, tmem_cols);
     }
 }
 
-size_t sketch_gemm_smem_bytes(int nacc, int npad, int a_stages, int o_stages) {
-    return make_layout(nacc, npad, a_stages, o_stages).total + 1024;
+size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages) {
+    return make_layout(nacc, npad / cg, a_stages, o_stages).total + 1024;
 }
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
 
-template <int NACC, int DIST, int MODE, bool FAST>
+template <int CG, int NACC, int DIST, int MODE, bool FAST>
 static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p, int grid,
                               size_t smem, cudaStream_t s) {
-    auto kern = sketch_gemm_kernel<NACC, DIST, MODE, FAST>;
+    auto kern = sketch_gemm_kernel<CG, NACC, DIST, MODE, FAST>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, smem, s>>>(tmA, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    // ablation bit 3: launch single-CTA tiles as clusters of 2 (isolates cluster placement effects)
+    attr[0].val.clusterDim.x = (CG == 1 && (p.ablate & 8u)) ? 2 : CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmA, p);
 }
 
-template <int NACC, int DIST>
+template <int CG, int NACC, int DIST>
 static cudaError_t dispatch_mode(const CUtensorMap& tmA, const SketchGemmParams& p, int mode,
                                  bool fast, int grid, size_t smem, cudaStream_t s) {
     if (mode == kTF32) {
-        if (DIST == kGaussian && fast) return launch_one<NACC, DIST, kTF32, true>(tmA, p, grid, smem, s);
-        return launch_one<NACC, DIST, kTF32, false>(tmA, p, grid, smem, s);
+        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kTF32, true>(tmA, p, grid, smem, s);
+        return launch_one<CG, NACC, DIST, kTF32, false>(tmA, p, grid, smem, s);
     }
     return cudaErrorNotSupported;
 }
 
-cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int nacc,
+template <int CG, int NACC>
+static cudaError_t dispatch_dist(const CUtensorMap& tmA, const SketchGemmParams& p, int dist,
+                                 int mode, bool fast, int grid, size_t smem, cudaStream_t s) {
+    if (dist == kGaussian) return dispatch_mode<CG, NACC, kGaussian>(tmA, p, mode, fast, grid, smem, s);
+    if (dist == kRademacher) return dispatch_mode<CG, NACC, kRademacher>(tmA, p, mode, fast, grid, smem, s);
+    return dispatch_mode<CG, NACC, kUniform>(tmA, p, mode, fast, grid, smem, s);
+}
+
+cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg, int nacc,
                                int dist, int mode, bool fast, int grid, size_t smem,
                                cudaStream_t s) {
-    if (nacc == 1) {
-        if (dist == kGaussian) return dispatch_mode<1, kGaussian>(tmA, p, mode, fast, grid, smem, s);
-        if (dist == kRademacher) return dispatch_mode<1, kRademacher>(tmA, p, mode, fast, grid, smem, s);
-        return dispatch_mode<1, kUniform>(tmA, p, mode, fast, grid, smem, s);
-    }
-    if (nacc == 2) {
-        if (dist == kGaussian) return dispatch_mode<2, kGaussian>(tmA, p, mode, fast, grid, smem, s);
-        if (dist == kRademacher) return dispatch_mode<2, kRademacher>(tmA, p, mode, fast, grid, smem, s);
-        return dispatch_mode<2, kUniform>(tmA, p, mode, fast, grid, smem, s);
-    }
+    if (cg == 1 && nacc == 1) return dispatch_dist<1, 1>(tmA, p, dist, mode, fast, grid, smem, s);
+    if (cg == 1 && nacc == 2) return dispatch_dist<1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
+    if (cg == 2 && nacc == 1) return dispatch_dist<2, 1>(tmA, p, dist, mode, fast, grid, smem, s);
+    if (cg == 2 && nacc == 2) return dispatch_dist<2, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     return cudaErrorNotSupported;
 }
 

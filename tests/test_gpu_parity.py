@@ -239,3 +239,19 @@ def test_error_codes():
     assert e.value.name == "SK_ERR_INVALID_VALUE"
     assert s.apply(A).abs().max().item() == 0.0
     assert s.apply(torch.zeros((0, 100), device="cuda")).shape == (0, 8)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("shape", [(1000, 3000, 256), (600, 1000, 48), (2049, 700, 128)])
+def test_cta_group_variants(cg, shape):
+    """Single-CTA tiles and CTA pairs (tcgen05 cta_group::2) agree with the oracle."""
+    sk = _sk()
+    n1, n2, r = shape
+    Ai = synth.int_matrix(11, n1, n2, -4, 4)
+    si = sk.Sketch(SEED, "rademacher", n2, r, cta_group=cg)
+    assert np.array_equal(si.apply(_dev(Ai)).cpu().numpy().astype(np.float64),
+                          oracle.sketch(SEED, "rademacher", Ai, r))
+    A = synth.uniform(12, n1, n2)
+    for omega in ("accurate", "fast"):
+        s = sk.Sketch(SEED, "gaussian", n2, r, cta_group=cg, omega=omega)
+        assert _relF(s.apply(_dev(A)).cpu().numpy(), oracle.sketch(SEED, "gaussian", A, r)) <= 5e-3
