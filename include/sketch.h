@@ -91,6 +91,10 @@ sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k);
  * tcgen05 cta_group::2 for n1 > 256), 1 = single-CTA tiles, 2 = CTA pairs when n1 > 256. */
 sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg);
 
+/* Core GEMM implementation: 0 = tcgen05 (default for r <= 256, tf32 operands), 1 = fp32 SIMT
+ * (used automatically for r > 256 or a B whose rows are not 16-byte aligned). */
+sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt);
+
 /* Performance ablation for measurements only (results are WRONG while set): bit 0 skips the
  * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs.  0 restores
  * normal operation. */

@@ -24,7 +24,7 @@ _OMEGA = {"accurate": 0, "fast": 1}
 
 EXPORTED_SYMBOLS = (
     "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
-    "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_ablation",
+    "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "sketch_generate", "sketch_generate_bits",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
@@ -70,6 +70,7 @@ def load_library(build_if_missing: bool = True):
         lib.sketch_set_split_k.argtypes = [vp, i32]
         lib.sketch_set_cta_group.argtypes = [vp, i32]
         lib.sketch_set_ablation.argtypes = [vp, ctypes.c_uint32]
+        lib.sketch_set_core_impl.argtypes = [vp, i32]
         lib.sketch_workspace_size.argtypes = [vp, i64, ctypes.POINTER(sz)]
         lib.sketch_apply.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, sz, vp]
         lib.nystrom_core.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
@@ -144,7 +145,8 @@ class Sketch:
     """
 
     def __init__(self, seed: int, dist, n2: int, r: int, mode: str = "tf32",
-                 omega: str = "accurate", split_k: int = 0, cta_group: int = 0):
+                 omega: str = "accurate", split_k: int = 0, cta_group: int = 0,
+                 core: str = "auto"):
         self._lib = load_library()
         self.seed, self.n2, self.r = int(seed), int(n2), int(r)
         self.dist = _DISTS[dist] if isinstance(dist, str) else int(dist)
@@ -156,6 +158,7 @@ class Sketch:
         _check(self._lib.sketch_set_omega_transform(h, _OMEGA[omega]))
         _check(self._lib.sketch_set_split_k(h, int(split_k)))
         _check(self._lib.sketch_set_cta_group(h, int(cta_group)))
+        _check(self._lib.sketch_set_core_impl(h, 1 if core == "simt" else 0))
         self._ws = {}
 
     def __del__(self):

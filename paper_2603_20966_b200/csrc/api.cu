@@ -27,6 +27,7 @@ struct sk_sketch_s {
     int omega_transform;
     int split_override;
     int cg_override;  // 0 auto, 1 force single-CTA tiles (ablation / tests)
+    int core_simt;    // 1: force the fp32 SIMT core GEMM (tests / ablation)
     uint32_t ablate;  // performance ablations (bench only): see SketchGemmParams::ablate
     int profiling;
     std::mutex prof_mu;
@@ -88,7 +89,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // 2D fp32 row-major tensor [rows x cols] with row stride ld (elements), box {box_cols, box_rows},
 // SWIZZLE_128B, out-of-bounds elements read as zero.
 sk_status_t make_map_2d(CUtensorMap* map, const float* base, int64_t rows, int64_t cols,
-                        int64_t ld, uint32_t box_cols, uint32_t box_rows) {
+                        int64_t ld, uint32_t box_cols, uint32_t box_rows, bool swizzle = true) {
     auto enc = get_encode();
     if (!enc) return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -97,7 +98,8 @@ sk_status_t make_map_2d(CUtensorMap* map, const float* base, int64_t rows, int64
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(SK_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(r) + ")");
@@ -178,12 +180,16 @@ size_t sketch_ws_bytes(const sk_sketch_s* h, int64_t n1, int64_t k) {
 }
 
 struct CorePlan {
+    bool tc;             // tcgen05 path (r <= 256) vs fp32 SIMT
     int chunks;
-    int chunk_rows;
+    int chunk_rows;      // SIMT: rows of B per chunk
+    int64_t base, step;  // tcgen05: 128-aligned chunk grid in global Omega rows
+    int npad, nacc;
 };
 
-CorePlan plan_core(const sk_sketch_s* h, int64_t m) {
+CorePlan plan_core_simt(const sk_sketch_s* h, int64_t m) {
     CorePlan C{};
+    C.tc = false;
     const int64_t tiles = ((h->r + 63) / 64) * ((h->r + 63) / 64);
     const int64_t want = std::max<int64_t>(1, (2 * sk::num_sms() + tiles - 1) / tiles);
     const int64_t maxc = std::max<int64_t>(1, (m + 31) / 32);
@@ -193,9 +199,25 @@ CorePlan plan_core(const sk_sketch_s* h, int64_t m) {
     return C;
 }
 
+// tcgen05 core for r <= 256 (one CTA per 128-aligned chunk of about m / #SMs rows); SIMT otherwise.
+CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0) {
+    if (h->r > 256 || h->core_simt) return plan_core_simt(h, m);
+    CorePlan C{};
+    C.tc = true;
+    C.npad = static_cast<int>(round_up(h->r, 16));
+    C.nacc = h->r > 128 ? 2 : 1;
+    C.base = i0 & ~static_cast<int64_t>(127);
+    const int64_t span = std::max<int64_t>(1, i0 + m - C.base);
+    const int64_t want = sk::num_sms();
+    C.step = round_up((span + want - 1) / want, 128);
+    C.chunks = static_cast<int>((span + C.step - 1) / C.step);
+    return C;
+}
+
 size_t core_ws_bytes(const sk_sketch_s* h, int64_t m) {
-    const CorePlan C = plan_core(h, m);
-    return static_cast<size_t>(C.chunks) * h->r * h->r * sizeof(float);
+    // chunk count of either plan for any block offset (an unaligned i0 adds at most one chunk)
+    const int64_t chunks = std::max<int64_t>(plan_core(h, m, 127).chunks + 1, plan_core_simt(h, m).chunks);
+    return static_cast<size_t>(chunks) * h->r * h->r * sizeof(float);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -274,7 +296,36 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
 // C[r x r] (ldc) = Omega[i0 : i0+m, :r]^T * B[m x r]
 sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, int64_t i0,
                       float* C, int64_t ldc, void* ws, cudaStream_t stream) {
-    const CorePlan CP = plan_core(h, m);
+    CorePlan CP = plan_core(h, m, i0);
+    if (CP.tc && (!aligned16(B) || (ldb & 3))) CP = plan_core_simt(h, m);  // TMA needs 16-B rows
+    if (CP.tc && m > 0) {
+        CUtensorMap map;
+        if (sk_status_t st = make_map_2d(&map, B, m, h->r, ldb, 32, 32, false)) return st;
+        sk::CoreTcParams q{};
+        q.part = static_cast<float*>(ws);
+        q.ldp = h->r;
+        q.i0 = i0;
+        q.base = CP.base;
+        q.step = CP.step;
+        q.m = static_cast<int32_t>(m);
+        q.r = static_cast<int32_t>(h->r);
+        q.npad = CP.npad;
+        q.nchunks = CP.chunks;
+        q.key0 = static_cast<uint32_t>(h->seed);
+        q.key1 = static_cast<uint32_t>(h->seed >> 32);
+        cudaError_t e;
+        {
+            LaunchScope ls(h, SK_PHASE_CORE_GEMM, stream);
+            e = sk::launch_core_gemm_tc(map, q, CP.nacc, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "core_gemm_tc launch");
+        {
+            LaunchScope ls(h, SK_PHASE_CORE_REDUCE, stream);
+            e = sk::launch_core_reduce(q.part, q.nchunks, q.r, C, ldc, stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "core_reduce launch");
+        return SK_SUCCESS;
+    }
     sk::CoreGemmParams p{};
     p.B = B;
     p.ldb = ldb;
@@ -338,6 +389,7 @@ sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, 
     h->omega_transform = SK_OMEGA_ACCURATE;
     h->split_override = 0;
     h->cg_override = 0;
+    h->core_simt = 0;
     h->ablate = 0;
     h->profiling = 0;
     *out = h;
@@ -410,6 +462,12 @@ sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
     if (cg < 0 || cg > 2) return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1 or 2");
     h->cg_override = cg;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    h->core_simt = simt ? 1 : 0;
     return SK_SUCCESS;
 }
 

@@ -109,3 +109,230 @@ cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaS
 }
 
 }  // namespace sk
+
+// =============================================================================================
+// tcgen05 core GEMM (r <= 256): one CTA per K-chunk of B rows computes the whole r x r partial.
+//   D[a, b] += OmegaT[a, i] * B[i, b]:  M = Omega columns a (NACC blocks of 128), N = npad (b),
+//   K = rows i in 32-row steps, kind::tf32, fp32 accumulators in TMEM.
+//   * Omega^T tile (A operand, K-major SW128) is regenerated by 16 producer warps with the sketch
+//     GEMM's tile writer (bit-identical Omega).
+//   * B tile: TMA loads row-major B (boxes of 32 rows x 32 columns, no swizzle) into a raw ring;
+//     the producer warps transpose it into a K-major SW128 tile (row b = 32 K-values), rounding to
+//     tf32 (RN) on the way.  (A transposed/MN-major tf32 operand produced zeros on sm_100a in
+//     tools/umma_test.cu, so B is made K-major in shared memory instead.)
+//   Chunks start at 128-aligned global Omega rows (the first may start before i0: those B rows
+//   are TMA zero-filled), so the generator always runs its aligned path.
+// =============================================================================================
+#include <cstdio>
+
+#include "omega_tile.cuh"
+#include "ptx.cuh"
+
+namespace sk {
+
+constexpr int kCoreCtl = 4, kCoreRng = 16;
+constexpr int kCoreThreads = (kCoreCtl + kCoreRng) * 32;
+constexpr int kCoreStages = 2;     // operand (Omega^T + B^T) ring
+constexpr int kCoreRawStages = 2;  // raw B ring (TMA)
+
+struct CoreSmem {
+    uint32_t raw_stage, o_stage, bt_stage, raw_off, o_off, bt_off, bar_off, total;
+};
+__host__ __device__ inline CoreSmem core_smem(int nacc, int npad) {
+    CoreSmem L;
+    L.raw_stage = static_cast<uint32_t>((npad + 31) / 32) * 4096u;
+    L.o_stage = static_cast<uint32_t>(nacc) * 16384u;
+    L.bt_stage = static_cast<uint32_t>(npad) * 128u;
+    L.raw_off = 0;
+    L.o_off = L.raw_off + kCoreRawStages * L.raw_stage;
+    L.bt_off = L.o_off + kCoreStages * L.o_stage;
+    L.bar_off = L.bt_off + kCoreStages * L.bt_stage;
+    L.total = L.bar_off + (2 * kCoreRawStages + 2 * kCoreStages + 2) * 8 + 16;
+    return L;
+}
+
+template <int NACC, int DIST, int MODE, bool FAST>
+__global__ void __launch_bounds__(kCoreThreads, 1)
+    core_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const CoreTcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    const CoreSmem L = core_smem(NACC, p.npad);
+    uint8_t* sRaw = smem + L.raw_off;
+    uint8_t* sO = smem + L.o_off;
+    uint8_t* sBt = smem + L.bt_off;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* full_raw = bars;
+    uint64_t* empty_raw = bars + kCoreRawStages;
+    uint64_t* full_op = bars + 2 * kCoreRawStages;
+    uint64_t* empty_op = full_op + kCoreStages;
+    uint64_t* done = empty_op + kCoreStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int chunk = blockIdx.x;
+    const int64_t g0 = p.base + static_cast<int64_t>(chunk) * p.step;  // aligned global row
+    const int64_t gend = min(p.i0 + static_cast<int64_t>(p.m), g0 + p.step);
+    const int ksteps = static_cast<int>((gend - g0 + 31) / 32);
+    uint32_t tmem_cols = 32;
+    while (tmem_cols < static_cast<uint32_t>(NACC * p.npad)) tmem_cols <<= 1;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kCoreRawStages; ++s) { mbar_init(&full_raw[s], 1); mbar_init(&empty_raw[s], kCoreRng); }
+        for (int s = 0; s < kCoreStages; ++s) { mbar_init(&full_op[s], kCoreRng); mbar_init(&empty_op[s], 1); }
+        mbar_init(done, 1);
+        fence_barrier_init();
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 2) tmem_alloc_rt(tmem_slot, tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            uint32_t st = 0, ph = 0;
+            const uint64_t pol = l2_policy_evict_first();
+            const int ngrp = (p.npad + 31) / 32;
+            for (int t = 0; t < ksteps; ++t) {
+                mbar_wait(&empty_raw[st], ph ^ 1);
+                mbar_arrive_expect_tx(&full_raw[st], L.raw_stage);
+                const int32_t row = static_cast<int32_t>(g0 - p.i0) + 32 * t;  // may be < 0: zero fill
+                for (int gcol = 0; gcol < ngrp; ++gcol)
+                    tma_load_2d(sRaw + st * L.raw_stage + gcol * 4096, &tmB, &full_raw[st], gcol * 32, row, pol);
+                if (++st == kCoreRawStages) { st = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            const uint32_t idesc = make_idesc(kFmtTF32, 128, static_cast<uint32_t>(p.npad), 0, 0);
+            uint32_t so = 0, po = 0;
+            for (int t = 0; t < ksteps; ++t) {
+                mbar_wait(&full_op[so], po);
+                tc_fence_after();
+                const uint32_t bt_base = smem_u32(sBt + so * L.bt_stage);
+                const uint32_t o_base = smem_u32(sO + so * L.o_stage);
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8) {
+                    const uint64_t bdesc = sw128_desc(bt_base + k8 * 32, 16, 1024);
+#pragma unroll
+                    for (int a = 0; a < NACC; ++a) {
+                        const uint64_t adesc = sw128_desc(o_base + a * 16384 + k8 * 32, 16, 1024);
+                        mma_tf32(tmem_base + a * p.npad, adesc, bdesc, idesc, (t > 0 || k8 > 0) ? 1u : 0u);
+                    }
+                }
+                mma_commit(&empty_op[so]);
+                if (++so == kCoreStages) { so = 0; po ^= 1; }
+            }
+            mma_commit(done);
+        }
+    } else if (warp >= kCoreCtl) {
+        const int tt = static_cast<int>(threadIdx.x) - kCoreCtl * 32;
+        const int nrows = 128 * NACC;  // Omega columns generated (a = 0 .. nrows-1)
+        const int n_start = tt % nrows, j_start = tt / nrows;
+        const int tq = (kCoreRng * 32) / nrows, tr = (kCoreRng * 32) % nrows;
+        uint32_t so = 0, po = 0, sr = 0, pr = 0;
+        for (int t = 0; t < ksteps; ++t) {
+            mbar_wait(&empty_op[so], po ^ 1);
+            uint8_t* o_tile = sO + so * L.o_stage;
+            if constexpr (DIST == kRademacher)
+                produce_omega_tile_r<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, 0, p.key0, p.key1, tt);
+            else
+                produce_omega_tile_g<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, 0, p.key0, p.key1,
+                                                       n_start, j_start, tq, tr);
+            // transpose the raw B tile (32 rows i x npad cols b, 128-B rows per 32-col group) into
+            // the K-major SW128 tile: row b, chunk j4 = rows 4 j4 .. 4 j4 + 3
+            mbar_wait(&full_raw[sr], pr);
+            const uint8_t* raw = sRaw + sr * L.raw_stage;
+            const uint32_t bt = smem_u32(sBt + so * L.bt_stage);
+            for (int c = tt; c < p.npad * 8; c += kCoreRng * 32) {
+                const int b = c % p.npad, j4 = c / p.npad;
+                const float* col = reinterpret_cast<const float*>(raw + (b >> 5) * 4096) + (b & 31);
+                float4 v = make_float4(col[(4 * j4 + 0) * 32], col[(4 * j4 + 1) * 32], col[(4 * j4 + 2) * 32],
+                                       col[(4 * j4 + 3) * 32]);
+                v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
+                const uint32_t addr = bt + static_cast<uint32_t>(b) * 128u +
+                                      ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(b & 7)) << 4);
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
+                             "f"(v.z), "f"(v.w)
+                             : "memory");
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty_raw[sr]);
+                mbar_arrive(&full_op[so]);
+            }
+            if (++so == kCoreStages) { so = 0; po ^= 1; }
+            if (++sr == kCoreRawStages) { sr = 0; pr ^= 1; }
+        }
+        if (tt < 128) {
+            const int q = tt >> 5;
+            mbar_wait(done, 0);
+            tc_fence_after();
+            float* out = p.part + static_cast<int64_t>(chunk) * p.r * p.ldp;
+#pragma unroll 1
+            for (int a = 0; a < NACC; ++a) {
+                const int row = a * 128 + q * 32 + static_cast<int>(lane);  // Omega column a
+                float* orow = out + static_cast<int64_t>(row) * p.ldp;
+#pragma unroll 1
+                for (int cc = 0; cc < p.npad; cc += 32) {
+                    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                           static_cast<uint32_t>(a * p.npad + cc);
+                    uint32_t v[32];
+                    if (cc + 32 <= p.npad) {
+                        tmem_ld_32x32b_x32(taddr, v);
+                    } else {
+                        uint32_t h[16];
+                        tmem_ld_32x32b_x16(taddr, h);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) { v[i] = h[i]; v[16 + i] = 0u; }
+                    }
+                    tmem_ld_wait();
+                    if (row < p.r) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (cc + i < p.r) orow[cc + i] = __uint_as_float(v[i]);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_rt(tmem_base, tmem_cols);
+    }
+}
+
+size_t core_gemm_tc_smem_bytes(int nacc, int npad) { return core_smem(nacc, npad).total + 1024; }
+
+template <int NACC, int DIST, int MODE, bool FAST>
+static cudaError_t launch_core_tc_one(const CUtensorMap& tmB, const CoreTcParams& p, cudaStream_t s) {
+    auto kern = core_gemm_tc_kernel<NACC, DIST, MODE, FAST>;
+    const size_t smem = core_gemm_tc_smem_bytes(NACC, p.npad);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<p.nchunks, kCoreThreads, smem, s>>>(tmB, p);
+    return cudaGetLastError();
+}
+
+template <int NACC>
+static cudaError_t core_tc_dist(const CUtensorMap& tmB, const CoreTcParams& p, int dist, bool fast,
+                                cudaStream_t s) {
+    if (dist == kRademacher) return launch_core_tc_one<NACC, kRademacher, kTF32, false>(tmB, p, s);
+    if (dist == kUniform) return launch_core_tc_one<NACC, kUniform, kTF32, false>(tmB, p, s);
+    if (fast) return launch_core_tc_one<NACC, kGaussian, kTF32, true>(tmB, p, s);
+    return launch_core_tc_one<NACC, kGaussian, kTF32, false>(tmB, p, s);
+}
+
+cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CoreTcParams& p, int nacc, int dist,
+                                bool fast, cudaStream_t s) {
+    if (nacc == 1) return core_tc_dist<1>(tmB, p, dist, fast, s);
+    if (nacc == 2) return core_tc_dist<2>(tmB, p, dist, fast, s);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace sk

@@ -46,6 +46,21 @@ struct CoreGemmParams {
     uint32_t key0, key1;
 };
 
+// tcgen05 core GEMM (r <= 256): chunk c covers global Omega rows
+// [max(i0, base + c*step), min(i0 + m, base + (c+1)*step)), base = i0 & ~127, step % 128 == 0.
+struct CoreTcParams {
+    float* part;          // nchunks x r x ldp partials
+    int64_t ldp;          // row stride of a partial (elements)
+    int64_t i0;           // global Omega row of B row 0
+    int64_t base;         // i0 rounded down to 128
+    int64_t step;         // rows per chunk (multiple of 128)
+    int32_t m;            // rows of B
+    int32_t r;
+    int32_t npad;         // MMA N (multiple of 16, <= 256)
+    int32_t nchunks;
+    uint32_t key0, key1;
+};
+
 struct LaunchCfg {
     int nacc;
     int split;
@@ -67,6 +82,9 @@ cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t
                                  int64_t ldo, cudaStream_t s);
 
 cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaStream_t s);
+cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CoreTcParams& p, int nacc, int dist,
+                                bool fast, cudaStream_t s);
+size_t core_gemm_tc_smem_bytes(int nacc, int npad);
 cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
                                int64_t ldc, cudaStream_t s);
 

@@ -19,6 +19,7 @@
 //               split-K partial).
 // Work unit = (m-block of 128*CG*NACC rows, K split s); units are dealt round-robin to CTA groups.
 #include "kernels.cuh"
+#include "omega_tile.cuh"
 #include "philox.cuh"
 #include "ptx.cuh"
 
@@ -44,118 +45,6 @@ __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stag
     L.bar_off = L.o_off + L.o_stage * o_stages;
     L.total = L.bar_off + (4 * kMaxStages + 4) * 8 + 16;
     return L;
-}
-
-// Omega tile for K-iteration `kit`: rows n in [0, npad) (Omega column c0+n), 32 K-values
-// (Omega rows kglob0 .. kglob0+31), K-major SW128: byte n*128 + ((j4 ^ (n&7)) << 4) + 4*e.
-// kglob0 = 128-aligned base + 32*kit + roff, roff in {0,1,2,3} (roff != 0 only for block calls
-// whose k0 is not a multiple of 4: then each 4-row chunk straddles two Philox calls).
-template <int DIST, int MODE, bool FAST>
-__device__ __forceinline__ void store_chunk(uint32_t addr, float4 v) {
-    if constexpr (MODE == kTF32) {
-        v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
-    }
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
-                 "f"(v.z), "f"(v.w)
-                 : "memory");
-}
-
-template <int DIST, bool FAST>
-__device__ __forceinline__ float4 values4(uint4 x) {
-    if constexpr (DIST == kUniform)
-        return make_float4(uniform_from_word(x.x), uniform_from_word(x.y), uniform_from_word(x.z),
-                           uniform_from_word(x.w));
-    else
-        return gauss4<FAST>(x);
-}
-
-__device__ __forceinline__ uint32_t pick_word(uint4 x, uint32_t sel) {
-    return sel == 0 ? x.x : sel == 1 ? x.y : sel == 2 ? x.z : x.w;
-}
-
-// Rademacher tile: one Philox call per column n = t serves all 32 K-values of the tile.
-template <int DIST, int MODE, bool FAST>
-__device__ __forceinline__ void produce_omega_tile_r(uint8_t* tile, int64_t kglob0, int roff,
-                                                     int npad, int c0, uint32_t key0,
-                                                     uint32_t key1, int t) {
-    if (t >= npad) return;
-    const int n = t;
-    const uint32_t col = static_cast<uint32_t>(c0 + n);
-    const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
-    const uint32_t sw = static_cast<uint32_t>(n & 7);
-    {
-        // bits for tile rows kk = 0..31: global rows kglob0 + kk
-        const uint64_t g = static_cast<uint64_t>(kglob0);
-        const uint4 x = philox_rade_call(g >> 7, col, key0, key1);
-        uint32_t w = pick_word(x, static_cast<uint32_t>(g >> 5) & 3u);
-        if (roff != 0) {
-            const uint64_t g2 = g + 32;  // next word: same call unless it crosses 128 rows
-            const uint4 x2 = ((g2 >> 7) == (g >> 7)) ? x : philox_rade_call(g2 >> 7, col, key0, key1);
-            const uint32_t w2 = pick_word(x2, static_cast<uint32_t>(g2 >> 5) & 3u);
-            w = __funnelshift_r(w, w2, static_cast<uint32_t>(g & 31));
-        }
-#pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 v = make_float4(rade_from_bit(w, 4 * j4 + 0), rade_from_bit(w, 4 * j4 + 1),
-                                         rade_from_bit(w, 4 * j4 + 2), rade_from_bit(w, 4 * j4 + 3));
-            store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v);
-        }
-    }
-}
-
-// Gaussian / uniform tile: the npad x 8 chunks (one Philox call -> 4 K-values each) are dealt to
-// the kRngThreads producers as c = t + kRngThreads * i, n = c % npad, j4 = c / npad, so a warp
-// stores 32 consecutive rows n at one j4 (conflict-free under the 128-B swizzle).
-template <int DIST, int MODE, bool FAST>
-__device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglob0, int roff,
-                                                     int npad, int c0, uint32_t key0,
-                                                     uint32_t key1, int n_start, int j_start,
-                                                     int tq, int tr) {
-    const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;
-    const uint32_t tile_base = smem_u32(tile);
-    int n = n_start, j4 = j_start;
-    if (roff == 0) {
-        // two independent chunks per iteration: their Philox / Box-Muller chains interleave
-#pragma unroll 1
-        while (j4 < 8) {
-            int n2 = n + tr, j2 = j4 + tq;
-            if (n2 >= npad) { n2 -= npad; ++j2; }
-            const bool two = j2 < 8;
-            const int n2c = two ? n2 : n, j2c = two ? j2 : j4;
-            const uint4 xa = philox_gauss_call(q0 + j4, static_cast<uint32_t>(c0 + n), key0, key1);
-            const uint4 xb = philox_gauss_call(q0 + j2c, static_cast<uint32_t>(c0 + n2c), key0, key1);
-            const float4 va = values4<DIST, FAST>(xa);
-            const float4 vb = values4<DIST, FAST>(xb);
-            store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n) * 128u +
-                                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4), va);
-            if (two)
-                store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n2) * 128u +
-                                                  ((static_cast<uint32_t>(j2) ^ static_cast<uint32_t>(n2 & 7)) << 4), vb);
-            n = n2 + tr;
-            j4 = j2 + tq;
-            if (n >= npad) { n -= npad; ++j4; }
-        }
-        return;
-    }
-#pragma unroll 1
-    for (; j4 < 8;) {
-        const uint32_t col = static_cast<uint32_t>(c0 + n);
-        const uint32_t addr = tile_base + static_cast<uint32_t>(n) * 128u +
-                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4);
-        // rows 4(q0+j4)+roff .. +3: tail of call q0+j4, head of call q0+j4+1
-        const float4 a0 = values4<DIST, FAST>(philox_gauss_call(q0 + j4, col, key0, key1));
-        const float4 a1 = values4<DIST, FAST>(philox_gauss_call(q0 + j4 + 1, col, key0, key1));
-        const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        float4 v;
-        v.x = roff == 1 ? a[1] : roff == 2 ? a[2] : a[3];
-        v.y = roff == 1 ? a[2] : roff == 2 ? a[3] : a[4];
-        v.z = roff == 1 ? a[3] : roff == 2 ? a[4] : a[5];
-        v.w = roff == 1 ? a[4] : roff == 2 ? a[5] : a[6];
-        store_chunk<DIST, MODE, FAST>(addr, v);
-        n += tr;
-        j4 += tq;
-        if (n >= npad) { n -= npad; ++j4; }
-    }
 }
 
 template <int CG, int NACC, int DIST, int MODE, bool FAST>
