@@ -144,7 +144,7 @@ class Sketch:
     mode: 'tf32x3' (fp32-accurate), 'tf32', 'bf16'; omega: 'accurate' | 'fast' Box-Muller.
     """
 
-    def __init__(self, seed: int, dist, n2: int, r: int, mode: str = "tf32",
+    def __init__(self, seed: int, dist, n2: int, r: int, mode: str = "tf32x3",
                  omega: str = "accurate", split_k: int = 0, cta_group: int = 0,
                  core: str = "auto"):
         self._lib = load_library()

@@ -134,25 +134,43 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     }
     P.cg = (n1 > 256 && h->cg_override != 1) ? 2 : 1;
     P.nacc = (n1 > 128 * P.cg) ? 2 : 1;
+    const bool x3 = h->mode == sk::kTF32x3;
+    const bool olo = x3 && h->dist != sk::kRademacher;
     // CTA pairs hand every Omega stage across the pair (relay + multicast commit): a deeper ring
-    // hides that round trip.
-    P.o_stages = (P.cg == 2) ? 4 : 2;
+    // hides that round trip in the fast modes; tf32x3 stages are 2-3x larger and MMA-bound.
+    P.o_stages = x3 ? 2 : ((P.cg == 2) ? 4 : 2);
     const int budget = sk::sketch_gemm_max_smem() - 2048;
+    auto ostage_bytes = [&](int nacc) {
+        const int otile = (npad_max / P.cg) * 128;
+        return (x3 ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
+    };
+    for (;;) {
+        const int a_stage = P.nacc * 128 * 32 * 4;
+        P.a_stages = std::min(6, (budget - P.o_stages * ostage_bytes(P.nacc)) / a_stage);
+        if (P.a_stages >= 2 || P.nacc == 1) break;
+        P.nacc = 1;  // tf32x3 single-CTA tiles: make room for >= 2 A stages
+    }
     const int a_stage = P.nacc * 128 * 32 * 4;
-    P.a_stages = std::min(6, (budget - P.o_stages * (npad_max / P.cg) * 128) / a_stage);
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages);
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo);
     P.kiters = static_cast<int>((k + kshift + 31) / 32);
     const int rows_per_unit = 128 * P.cg * P.nacc;
     P.num_mblk = static_cast<int>((n1 + rows_per_unit - 1) / rows_per_unit);
     P.ws_per_split = static_cast<size_t>(n1) * npad_max * sizeof(float);
     const int nsm = sk::num_sms() / P.cg;  // independent workers (CTAs or CTA pairs)
+    // The tensor core accumulates fp32 in TMEM with a bias toward zero of ~2^-24 per K=8 MMA step
+    // (measured: relF = 7e-9 x K per accumulator, tools/acc_test.py).  tf32x3 promises fp32
+    // accuracy (1e-5), so it caps K per accumulator at 1024 (32 K-iterations) with split-K; the
+    // partials are summed in fp32 round-to-nearest.
+    const int min_split = x3 ? (P.kiters + 31) / 32 : 1;
     int best_s = 1;
     if (h->split_override > 0) {
         best_s = std::min(h->split_override, std::max(1, P.kiters));
+    } else if (min_split > 64) {
+        best_s = min_split;
     } else {
         double best = 1e300;
         const double unit_ovh = 2.0;  // epilogue + pipeline fill, in K-iteration units
-        for (int s = 1; s <= std::min(64, std::max(1, P.kiters / 4)); ++s) {
+        for (int s = min_split; s <= std::max(min_split, std::min(64, std::max(1, P.kiters / 4))); ++s) {
             const int64_t units = static_cast<int64_t>(P.num_mblk) * s;
             const int64_t waves = (units + nsm - 1) / nsm;
             const int kper = (P.kiters + s - 1) / s;
@@ -201,7 +219,8 @@ CorePlan plan_core_simt(const sk_sketch_s* h, int64_t m) {
 
 // tcgen05 core for r <= 256 (one CTA per 128-aligned chunk of about m / #SMs rows); SIMT otherwise.
 CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0) {
-    if (h->r > 256 || h->core_simt) return plan_core_simt(h, m);
+    // tf32x3 keeps C fp32-accurate with the fp32-FMA core (a 3xTF32 core is future work)
+    if (h->r > 256 || h->core_simt || h->mode == sk::kTF32x3) return plan_core_simt(h, m);
     CorePlan C{};
     C.tc = true;
     C.npad = static_cast<int>(round_up(h->r, 16));
@@ -228,8 +247,8 @@ sk_status_t check_handle(const sk_sketch_s* h) {
 }
 
 sk_status_t check_mode(const sk_sketch_s* h) {
-    if (h->mode != sk::kTF32)
-        return fail(SK_ERR_UNSUPPORTED, "this build implements SK_MODE_TF32 only");
+    if (h->mode == sk::kBF16)
+        return fail(SK_ERR_UNSUPPORTED, "SK_MODE_BF16 is not implemented in this build");
     if (h->omega_transform == SK_OMEGA_FAST && h->mode == sk::kTF32x3)
         return fail(SK_ERR_UNSUPPORTED, "SK_OMEGA_FAST is not allowed with SK_MODE_TF32X3");
     return SK_SUCCESS;
@@ -385,7 +404,7 @@ sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, 
     h->dist = static_cast<int>(dist);
     h->n2 = n2;
     h->r = r;
-    h->mode = sk::kTF32;
+    h->mode = sk::kTF32x3;
     h->omega_transform = SK_OMEGA_ACCURATE;
     h->split_override = 0;
     h->cg_override = 0;

@@ -74,7 +74,8 @@ struct LaunchCfg {
 cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg,
                                int nacc, int dist, int mode, bool fast, int grid, size_t smem,
                                cudaStream_t s);
-size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages);
+size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool x3,
+                              bool olo);
 int sketch_gemm_max_smem();
 
 cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,

@@ -16,14 +16,24 @@ namespace sk {
 // (Omega rows kglob0 .. kglob0+31), K-major SW128: byte n*128 + ((j4 ^ (n&7)) << 4) + 4*e.
 // kglob0 = 128-aligned base + 32*kit + roff, roff in {0,1,2,3} (roff != 0 only for block calls
 // whose k0 is not a multiple of 4: then each 4-row chunk straddles two Philox calls).
-template <int DIST, int MODE, bool FAST>
-__device__ __forceinline__ void store_chunk(uint32_t addr, float4 v) {
-    if constexpr (MODE == kTF32) {
-        v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
-    }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w)
                  : "memory");
+}
+
+// tf32 mode: Omega rounded RN to tf32.  tf32x3 mode: Omega_hi = tf32_rn(w) at addr and
+// Omega_lo = w - Omega_hi (exact in fp32) at addr + lo_off (Rademacher: +-1 is exact, no lo tile).
+template <int DIST, int MODE, bool FAST>
+__device__ __forceinline__ void store_chunk(uint32_t addr, float4 v, uint32_t lo_off = 0) {
+    if constexpr (MODE == kTF32 || MODE == kTF32x3) {
+        const float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
+        st_shared_v4(addr, h);
+        if constexpr (MODE == kTF32x3 && DIST != kRademacher)
+            st_shared_v4(addr + lo_off, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
+    } else {
+        st_shared_v4(addr, v);
+    }
 }
 
 template <int DIST, bool FAST>
@@ -43,7 +53,7 @@ __device__ __forceinline__ uint32_t pick_word(uint4 x, uint32_t sel) {
 template <int DIST, int MODE, bool FAST>
 __device__ __forceinline__ void produce_omega_tile_r(uint8_t* tile, int64_t kglob0, int roff,
                                                      int npad, int c0, uint32_t key0,
-                                                     uint32_t key1, int t) {
+                                                     uint32_t key1, int t, uint32_t lo_off = 0) {
     if (t >= npad) return;
     const int n = t;
     const uint32_t col = static_cast<uint32_t>(c0 + n);
@@ -64,7 +74,7 @@ __device__ __forceinline__ void produce_omega_tile_r(uint8_t* tile, int64_t kglo
         for (int j4 = 0; j4 < 8; ++j4) {
             const float4 v = make_float4(rade_from_bit(w, 4 * j4 + 0), rade_from_bit(w, 4 * j4 + 1),
                                          rade_from_bit(w, 4 * j4 + 2), rade_from_bit(w, 4 * j4 + 3));
-            store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v);
+            store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v, lo_off);
         }
     }
 }
@@ -76,7 +86,7 @@ template <int DIST, int MODE, bool FAST>
 __device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglob0, int roff,
                                                      int npad, int c0, uint32_t key0,
                                                      uint32_t key1, int n_start, int j_start,
-                                                     int tq, int tr) {
+                                                     int tq, int tr, uint32_t lo_off = 0) {
     const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;
     const uint32_t tile_base = smem_u32(tile);
     int n = n_start, j4 = j_start;
@@ -93,10 +103,10 @@ __device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglo
             const float4 va = values4<DIST, FAST>(xa);
             const float4 vb = values4<DIST, FAST>(xb);
             store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n) * 128u +
-                                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4), va);
+                                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4), va, lo_off);
             if (two)
                 store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n2) * 128u +
-                                                  ((static_cast<uint32_t>(j2) ^ static_cast<uint32_t>(n2 & 7)) << 4), vb);
+                                                  ((static_cast<uint32_t>(j2) ^ static_cast<uint32_t>(n2 & 7)) << 4), vb, lo_off);
             n = n2 + tr;
             j4 = j2 + tq;
             if (n >= npad) { n -= npad; ++j4; }
@@ -117,7 +127,7 @@ __device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglo
         v.y = roff == 1 ? a[2] : roff == 2 ? a[3] : a[4];
         v.z = roff == 1 ? a[3] : roff == 2 ? a[4] : a[5];
         v.w = roff == 1 ? a[4] : roff == 2 ? a[5] : a[6];
-        store_chunk<DIST, MODE, FAST>(addr, v);
+        store_chunk<DIST, MODE, FAST>(addr, v, lo_off);
         n += tr;
         j4 += tq;
         if (n >= npad) { n -= npad; ++j4; }

@@ -32,14 +32,21 @@ constexpr int kRngThreads = kRngWarps * 32;
 constexpr uint32_t kATileBytes = 128 * 32 * 4;  // one 128-row x 32-fp32 TMA box
 constexpr int kMaxStages = 8;
 
+// Operand ring stage: [A_lo tile (tf32x3 only)] [Omega_hi tile] [Omega_lo tile (tf32x3, Gaussian/uniform)]
 struct SmemLayout {
     uint32_t a_stage, o_stage, a_off, o_off, bar_off, total;
+    uint32_t alo_off, ohi_off, olo_off;  // offsets inside an operand stage
 };
 
-__host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stages, int o_stages) {
+__host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stages, int o_stages,
+                                                  bool x3 = false, bool olo = false) {
     SmemLayout L;
     L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes;
-    L.o_stage = static_cast<uint32_t>(npad) * 128u;
+    const uint32_t otile = static_cast<uint32_t>(npad) * 128u;
+    L.alo_off = 0;
+    L.ohi_off = x3 ? L.a_stage : 0u;
+    L.olo_off = L.ohi_off + otile;
+    L.o_stage = L.ohi_off + otile * (olo ? 2u : 1u);
     L.a_off = 0;
     L.o_off = L.a_off + L.a_stage * a_stages;
     L.bar_off = L.o_off + L.o_stage * o_stages;
@@ -53,8 +60,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
+    constexpr bool X3 = (MODE == kTF32x3);                 // 3xTF32: A_lo and Omega_lo operands
+    constexpr bool OLO = X3 && (DIST != kRademacher);      // +-1 is exact in tf32: no Omega_lo
+    constexpr bool ARELAY = (CG == 2) && X3;               // peer A lands on its own barrier
     const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
-    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages);
+    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, X3, OLO);
     uint8_t* sA = smem + L.a_off;
     uint8_t* sO = smem + L.o_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -78,8 +88,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         // full_a: one expect_tx arrival; with CG = 2 the leader's barrier counts the bytes of BOTH
         // CTAs' TMA loads (the peer's loads complete_tx on it directly)
+        // (tf32x3 pairs: each CTA's A lands on its own barrier -- its producers read it to form
+        // A_lo -- and the peer's completion is relayed to the leader: leader count 2)
         for (int s = 0; s < p.a_stages; ++s) {
-            mbar_init(&full_a[s], 1);
+            mbar_init(&full_a[s], 1 + ((ARELAY && leader) ? 1 : 0));
             mbar_init(&empty_a[s], 1);
         }
         for (int s = 0; s < p.o_stages; ++s) {
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
                         continue;
                     }
-                    if constexpr (CG == 2) {
+                    if constexpr (CG == 2 && !ARELAY) {
                         // both CTAs load their own rows; bytes are counted on the leader's barrier
                         const uint32_t bar = mapa_shared(smem_u32(&full_a[st]), 0);
                         if (leader) mbar_arrive_expect_tx(&full_a[st], 2 * a_bytes_cta);
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int a = 0; a < NACC; ++a)
                             tma_load_2d(sA + st * L.a_stage + a * kATileBytes, &tmA, &full_a[st], x,
-                                        mb * rows_per_unit + a * 128, pol);
+                                        mb * rows_per_unit + a * 128 * CG + static_cast<int>(crank) * 128, pol);
                     }
                     if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
                 }
@@ -159,13 +171,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t o_base = smem_u32(sO + so * L.o_stage);
 #pragma unroll
                     for (int k8 = 0; k8 < ((p.ablate & 4u) ? 0 : 4); ++k8) {
-                        const uint64_t bdesc = sw128_desc(o_base + k8 * 32, 16, 1024);
+                        const uint64_t bdesc = sw128_desc(o_base + L.ohi_off + k8 * 32, 16, 1024);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a) {
                             const uint64_t adesc = sw128_desc(a_base + a * kATileBytes + k8 * 32, 16, 1024);
-                            const uint32_t acc = (kit > kb || k8 > 0) ? 1u : 0u;
-                            if constexpr (CG == 2) mma_tf32_pair(tmem_base + a * p.npad, adesc, bdesc, idesc, acc);
-                            else mma_tf32(tmem_base + a * p.npad, adesc, bdesc, idesc, acc);
+                            uint32_t acc = (kit > kb || k8 > 0) ? 1u : 0u;
+                            const uint32_t d = tmem_base + a * p.npad;
+                            if constexpr (X3) {
+                                // small terms first: A_lo * Omega_hi, A_hi * Omega_lo, then A_hi * Omega_hi
+                                const uint64_t alo = sw128_desc(o_base + L.alo_off + a * kATileBytes + k8 * 32, 16, 1024);
+                                if constexpr (CG == 2) mma_tf32_pair(d, alo, bdesc, idesc, acc);
+                                else mma_tf32(d, alo, bdesc, idesc, acc);
+                                acc = 1u;
+                                if constexpr (OLO) {
+                                    const uint64_t blo = sw128_desc(o_base + L.olo_off + k8 * 32, 16, 1024);
+                                    if constexpr (CG == 2) mma_tf32_pair(d, adesc, blo, idesc, acc);
+                                    else mma_tf32(d, adesc, blo, idesc, acc);
+                                }
+                            }
+                            if constexpr (CG == 2) mma_tf32_pair(d, adesc, bdesc, idesc, acc);
+                            else mma_tf32(d, adesc, bdesc, idesc, acc);
                         }
                     }
                     if constexpr (CG == 2) {
@@ -187,9 +212,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The peer's producer warps arrive on its LOCAL full_o (cheap, CTA scope); one thread
         // (warp 2) forwards a single release.cluster arrive per stage to the leader's full_o,
         // keeping the cluster-scope fence off the producers' critical path.
-        if (CG == 2 && !leader && warp == 2 && elect_one()) {
-            uint64_t* bars_r = full_o;
-            const uint32_t nst = static_cast<uint32_t>(p.o_stages);
+        if (CG == 2 && !leader && (warp == 2 || ARELAY) && elect_one()) {
+            uint64_t* bars_r = (warp == 2) ? full_o : full_a;  // warp 3 relays A (tf32x3 pairs)
+            const uint32_t nst = static_cast<uint32_t>((warp == 2) ? p.o_stages : p.a_stages);
             uint32_t st = 0, ph = 0;
             for (int u = group; u < total_units; u += ngroups) {
                 const int s = u - (u / p.split) * p.split;
@@ -208,23 +233,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_start = t % npad_loc, j_start = t / npad_loc;
         const int tq = kRngThreads / npad_loc, tr = kRngThreads % npad_loc;
         const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc;
-        uint32_t so = 0, po = 0, local = 0;
+        uint32_t so = 0, po = 0, sa = 0, pa = 0, local = 0;
+        const uint32_t lo_off = L.olo_off - L.ohi_off;
         for (int u = group; u < total_units; u += ngroups, ++local) {
             const int mb = u / p.split, s = u - (u / p.split) * p.split;
             const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
             for (int kit = kb; kit < ke; ++kit) {
                 mbar_wait(&empty_o[so], po ^ 1);
+                uint8_t* ostage = sO + so * L.o_stage;
                 if (p.ablate & 1u) {
                     // ablation: stage marked full without generating Omega
                 } else if constexpr (DIST == kRademacher)
-                    produce_omega_tile_r<DIST, MODE, FAST>(sO + so * L.o_stage,
+                    produce_omega_tile_r<DIST, MODE, FAST>(ostage + L.ohi_off,
                                                            p.k0a + static_cast<int64_t>(kit) * 32,
-                                                           p.roff, npad_loc, c0_loc, p.key0, p.key1, t);
+                                                           p.roff, npad_loc, c0_loc, p.key0, p.key1, t, lo_off);
                 else
-                    produce_omega_tile_g<DIST, MODE, FAST>(sO + so * L.o_stage,
+                    produce_omega_tile_g<DIST, MODE, FAST>(ostage + L.ohi_off,
                                                            p.k0a + static_cast<int64_t>(kit) * 32,
                                                            p.roff, npad_loc, c0_loc, p.key0, p.key1,
-                                                           n_start, j_start, tq, tr);
+                                                           n_start, j_start, tq, tr, lo_off);
+                if constexpr (X3) {
+                    // A_lo = A - trunc_tf32(A) (exact), elementwise over this CTA's A tile: the A tile
+                    // and A_lo share the SW128 layout, so the copy is layout-agnostic
+                    mbar_wait(&full_a[sa], pa);
+                    const float4* src = reinterpret_cast<const float4*>(sA + sa * L.a_stage);
+                    float4* dst = reinterpret_cast<float4*>(ostage + L.alo_off);
+                    for (int i = t; i < static_cast<int>(L.a_stage / 16); i += kRngThreads) {
+                        float4 v = src[i];
+                        v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                        v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                        v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                        v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                        dst[i] = v;
+                    }
+                    if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
+                }
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full_o[so]);
@@ -290,8 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages) {
-    return make_layout(nacc, npad / cg, a_stages, o_stages).total + 1024;
+size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool x3, bool olo) {
+    return make_layout(nacc, npad / cg, a_stages, o_stages, x3, olo).total + 1024;
 }
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
@@ -326,6 +369,7 @@ static cudaError_t dispatch_mode(const CUtensorMap& tmA, const SketchGemmParams&
         if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kTF32, true>(tmA, p, grid, smem, s);
         return launch_one<CG, NACC, DIST, kTF32, false>(tmA, p, grid, smem, s);
     }
+    if (mode == kTF32x3) return launch_one<CG, NACC, DIST, kTF32x3, false>(tmA, p, grid, smem, s);
     return cudaErrorNotSupported;
 }
 
