@@ -135,24 +135,27 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     P.cg = (n1 > 256 && h->cg_override != 1) ? 2 : 1;
     P.nacc = (n1 > 128 * P.cg) ? 2 : 1;
     const bool x3 = h->mode == sk::kTF32x3;
+    const bool bf = h->mode == sk::kBF16;
+    const bool xa = x3 || bf;
+    const int ks = bf ? 64 : 32;
     const bool olo = x3 && h->dist != sk::kRademacher;
     // CTA pairs hand every Omega stage across the pair (relay + multicast commit): a deeper ring
     // hides that round trip in the fast modes; tf32x3 stages are 2-3x larger and MMA-bound.
-    P.o_stages = x3 ? 2 : ((P.cg == 2) ? 4 : 2);
+    P.o_stages = xa ? 2 : ((P.cg == 2) ? 4 : 2);
     const int budget = sk::sketch_gemm_max_smem() - 2048;
     auto ostage_bytes = [&](int nacc) {
         const int otile = (npad_max / P.cg) * 128;
-        return (x3 ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
+        return (xa ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
     };
     for (;;) {
-        const int a_stage = P.nacc * 128 * 32 * 4;
+        const int a_stage = P.nacc * 128 * ks * 4;
         P.a_stages = std::min(6, (budget - P.o_stages * ostage_bytes(P.nacc)) / a_stage);
         if (P.a_stages >= 2 || P.nacc == 1) break;
         P.nacc = 1;  // tf32x3 single-CTA tiles: make room for >= 2 A stages
     }
-    const int a_stage = P.nacc * 128 * 32 * 4;
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo);
-    P.kiters = static_cast<int>((k + kshift + 31) / 32);
+    const int a_stage = P.nacc * 128 * ks * 4;
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, xa, olo, ks);
+    P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
     const int rows_per_unit = 128 * P.cg * P.nacc;
     P.num_mblk = static_cast<int>((n1 + rows_per_unit - 1) / rows_per_unit);
     P.ws_per_split = static_cast<size_t>(n1) * npad_max * sizeof(float);
@@ -247,8 +250,6 @@ sk_status_t check_handle(const sk_sketch_s* h) {
 }
 
 sk_status_t check_mode(const sk_sketch_s* h) {
-    if (h->mode == sk::kBF16)
-        return fail(SK_ERR_UNSUPPORTED, "SK_MODE_BF16 is not implemented in this build");
     if (h->omega_transform == SK_OMEGA_FAST && h->mode == sk::kTF32x3)
         return fail(SK_ERR_UNSUPPORTED, "SK_OMEGA_FAST is not allowed with SK_MODE_TF32X3");
     return SK_SUCCESS;

@@ -20,7 +20,7 @@ struct SketchGemmParams {
                           // needs 16-byte inner coordinates); negative columns -> TMA zero fill
     int32_t roff;         // k0a % 4 (0 except for unaligned block calls)
     int32_t n1;           // rows of A
-    int32_t kiters;       // number of 32-wide K iterations
+    int32_t kiters;       // number of K iterations (32 wide; 64 wide in bf16 mode)
     int32_t r_valid;      // columns of this pass to store (<= npad)
     int32_t c0;           // global Omega column of accumulator column 0
     int32_t npad;         // MMA N (multiple of 16, <= 256)
@@ -74,8 +74,8 @@ struct LaunchCfg {
 cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg,
                                int nacc, int dist, int mode, bool fast, int grid, size_t smem,
                                cudaStream_t s);
-size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool x3,
-                              bool olo);
+size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa,
+                              bool olo, int ks);
 int sketch_gemm_max_smem();
 
 cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,

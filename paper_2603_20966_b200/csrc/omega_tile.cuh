@@ -134,4 +134,78 @@ __device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglo
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// bf16 tiles: one 64-row K-step, row n (Omega column c0 + n) = 64 bf16 = 128 B, 16-byte chunk
+// j8 (K-values 8 j8 .. 8 j8 + 7) at n*128 + ((j8 ^ (n & 7)) << 4); values rounded RN to bf16.
+// kglob0 = 128-aligned base + 64 * kit + roff.
+template <int DIST, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_bf16_r(uint8_t* tile, int64_t kglob0, int roff,
+                                                          int npad, int c0, uint32_t key0,
+                                                          uint32_t key1, int t) {
+    (void)roff;
+    if (t >= npad) return;
+    const int n = t;
+    const uint32_t col = static_cast<uint32_t>(c0 + n);
+    const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
+    const uint32_t sw = static_cast<uint32_t>(n & 7);
+    // 64 bits for rows kglob0 .. kglob0 + 63, bit b of the 64 = row kglob0 + b
+    const uint64_t g = static_cast<uint64_t>(kglob0);
+    const uint4 x = philox_rade_call(g >> 7, col, key0, key1);
+    const uint32_t sel = static_cast<uint32_t>(g >> 5) & 3u;
+    uint32_t w0 = pick_word(x, sel), w1, w2;
+    if (sel < 3) {
+        w1 = pick_word(x, sel + 1);
+        w2 = (sel < 2) ? pick_word(x, sel + 2) : pick_word(philox_rade_call((g >> 7) + 1, col, key0, key1), 0);
+    } else {
+        const uint4 x2 = philox_rade_call((g >> 7) + 1, col, key0, key1);
+        w1 = x2.x;
+        w2 = x2.y;
+    }
+    const uint32_t sh = static_cast<uint32_t>(g & 31);
+    const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+#pragma unroll
+    for (int j8 = 0; j8 < 8; ++j8) {
+        const uint32_t w = (j8 < 4) ? lo : hi;
+        const int b0 = (j8 & 3) * 8;
+        // bf16 +1 = 0x3F80, -1 = 0xBF80
+        uint32_t q[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t s0 = (w >> (b0 + 2 * e)) & 1u, s1 = (w >> (b0 + 2 * e + 1)) & 1u;
+            q[e] = (0x3F80u | (s0 << 15)) | ((0x3F80u | (s1 << 15)) << 16);
+        }
+        st_shared_v4_u32(row_base + ((static_cast<uint32_t>(j8) ^ sw) << 4), q[0], q[1], q[2], q[3]);
+    }
+}
+
+template <int DIST, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_bf16_g(uint8_t* tile, int64_t kglob0, int roff,
+                                                          int npad, int c0, uint32_t key0,
+                                                          uint32_t key1, int n_start, int j_start,
+                                                          int tq, int tr) {
+    const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;  // call holding row kglob0 - roff
+    const uint32_t tile_base = smem_u32(tile);
+    int n = n_start, j8 = j_start;
+#pragma unroll 1
+    while (j8 < 8) {
+        const uint32_t col = static_cast<uint32_t>(c0 + n);
+        const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8, col, key0, key1));
+        const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8 + 1, col, key0, key1));
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        if (roff != 0) {
+            const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8 + 2, col, key0, key1));
+            const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
+        }
+        st_shared_v4_u32(tile_base + static_cast<uint32_t>(n) * 128u +
+                             ((static_cast<uint32_t>(j8) ^ static_cast<uint32_t>(n & 7)) << 4),
+                         pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                         pack_bf16x2(v[6], v[7]));
+        n += tr;
+        j8 += tq;
+        if (n >= npad) { n -= npad; ++j8; }
+    }
+}
+
 }  // namespace sk

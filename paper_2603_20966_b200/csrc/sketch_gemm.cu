@@ -38,13 +38,16 @@ struct SmemLayout {
     uint32_t alo_off, ohi_off, olo_off;  // offsets inside an operand stage
 };
 
+// ks: K per pipeline step (32 for tf32 / tf32x3, 64 for bf16: a bf16 swizzle row holds 64 values).
+// xa: the producers write a transformed A operand tile (tf32x3: A_lo fp32; bf16: A in bf16), which
+// takes nacc * 16 KB in the operand stage in both cases.
 __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stages, int o_stages,
-                                                  bool x3 = false, bool olo = false) {
+                                                  bool xa = false, bool olo = false, int ks = 32) {
     SmemLayout L;
-    L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes;
+    L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes * static_cast<uint32_t>(ks / 32);
     const uint32_t otile = static_cast<uint32_t>(npad) * 128u;
     L.alo_off = 0;
-    L.ohi_off = x3 ? L.a_stage : 0u;
+    L.ohi_off = xa ? static_cast<uint32_t>(nacc) * kATileBytes : 0u;
     L.olo_off = L.ohi_off + otile;
     L.o_stage = L.ohi_off + otile * (olo ? 2u : 1u);
     L.a_off = 0;
@@ -61,10 +64,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     constexpr bool X3 = (MODE == kTF32x3);                 // 3xTF32: A_lo and Omega_lo operands
+    constexpr bool BF = (MODE == kBF16);                   // bf16 operands, K = 16 per MMA
+    constexpr bool XA = X3 || BF;                          // producers transform A in smem
     constexpr bool OLO = X3 && (DIST != kRademacher);      // +-1 is exact in tf32: no Omega_lo
-    constexpr bool ARELAY = (CG == 2) && X3;               // peer A lands on its own barrier
+    constexpr bool ARELAY = (CG == 2) && XA;               // peer A lands on its own barrier
+    constexpr int KS = BF ? 64 : 32;                       // K per pipeline step
+    constexpr int NBOX = KS / 32;                          // 128-B TMA boxes per accumulator
     const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
-    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, X3, OLO);
+    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, XA, OLO, KS);
     uint8_t* sA = smem + L.a_off;
     uint8_t* sO = smem + L.o_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
                 for (int kit = kb; kit < ke; ++kit) {
                     mbar_wait(&empty_a[st], ph ^ 1);
-                    const int x = kit * 32 - p.kshift;
+                    const int x = kit * KS - p.kshift;
                     if (p.ablate & 2u) {  // ablation: no A traffic, stage marked full at once
                         if (leader) mbar_arrive(&full_a[st]);
                         if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
@@ -140,14 +147,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (leader) mbar_arrive_expect_tx(&full_a[st], 2 * a_bytes_cta);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a)
-                            tma_load_2d_pair(sA + st * L.a_stage + a * kATileBytes, &tmA, bar, x,
+                            tma_load_2d_pair(sA + st * L.a_stage + a * kATileBytes * NBOX, &tmA, bar, x,
                                              mb * rows_per_unit + a * 256 + static_cast<int>(crank) * 128, pol);
                     } else {
                         mbar_arrive_expect_tx(&full_a[st], a_bytes_cta);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a)
-                            tma_load_2d(sA + st * L.a_stage + a * kATileBytes, &tmA, &full_a[st], x,
-                                        mb * rows_per_unit + a * 128 * CG + static_cast<int>(crank) * 128, pol);
+#pragma unroll
+                            for (int bx = 0; bx < NBOX; ++bx)
+                                tma_load_2d(sA + st * L.a_stage + (a * NBOX + bx) * kATileBytes, &tmA, &full_a[st],
+                                            x + 32 * bx, mb * rows_per_unit + a * 128 * CG + static_cast<int>(crank) * 128, pol);
                     }
                     if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
                 }
@@ -156,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer (leader)
         if (leader && elect_one()) {
-            const uint32_t idesc = make_idesc(kFmtTF32, 128 * CG, static_cast<uint32_t>(p.npad), 0, 0);
+            const uint32_t idesc = make_idesc(BF ? kFmtBF16 : kFmtTF32, 128 * CG, static_cast<uint32_t>(p.npad), 0, 0);
             uint32_t sa = 0, pa = 0, so = 0, po = 0, local = 0;
             for (int u = group; u < total_units; u += ngroups, ++local) {
                 const int s = u - (u / p.split) * p.split;
@@ -189,8 +198,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     else mma_tf32(d, adesc, blo, idesc, acc);
                                 }
                             }
-                            if constexpr (CG == 2) mma_tf32_pair(d, adesc, bdesc, idesc, acc);
-                            else mma_tf32(d, adesc, bdesc, idesc, acc);
+                            if constexpr (BF) {
+                                // bf16 A tile (converted by the producers) in the operand stage
+                                const uint64_t abf = sw128_desc(o_base + L.alo_off + a * kATileBytes + k8 * 32, 16, 1024);
+                                if constexpr (CG == 2) mma_bf16_pair(d, abf, bdesc, idesc, acc);
+                                else mma_bf16(d, abf, bdesc, idesc, acc);
+                            } else {
+                                if constexpr (CG == 2) mma_tf32_pair(d, adesc, bdesc, idesc, acc);
+                                else mma_tf32(d, adesc, bdesc, idesc, acc);
+                            }
                         }
                     }
                     if constexpr (CG == 2) {
@@ -243,6 +259,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* ostage = sO + so * L.o_stage;
                 if (p.ablate & 1u) {
                     // ablation: stage marked full without generating Omega
+                } else if constexpr (BF) {
+                    if constexpr (DIST == kRademacher)
+                        produce_omega_tile_bf16_r<DIST, FAST>(ostage + L.ohi_off, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                              p.roff, npad_loc, c0_loc, p.key0, p.key1, t);
+                    else
+                        produce_omega_tile_bf16_g<DIST, FAST>(ostage + L.ohi_off, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                              p.roff, npad_loc, c0_loc, p.key0, p.key1,
+                                                              n_start, j_start, tq, tr);
                 } else if constexpr (DIST == kRademacher)
                     produce_omega_tile_r<DIST, MODE, FAST>(ostage + L.ohi_off,
                                                            p.k0a + static_cast<int64_t>(kit) * 32,
@@ -252,6 +276,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                            p.k0a + static_cast<int64_t>(kit) * 32,
                                                            p.roff, npad_loc, c0_loc, p.key0, p.key1,
                                                            n_start, j_start, tq, tr, lo_off);
+                if constexpr (BF) {
+                    // A (two fp32 SW128 boxes of 32 K per accumulator) -> one bf16 SW128 tile of 64 K:
+                    // item (acc a, row m, chunk j8 = 8 K-values); a warp covers 32 consecutive rows
+                    mbar_wait(&full_a[sa], pa);
+                    const uint32_t src0 = smem_u32(sA + sa * L.a_stage);
+                    const uint32_t dst0 = smem_u32(ostage + L.alo_off);
+                    for (int i = t; i < NACC * 1024; i += kRngThreads) {
+                        const int a = i >> 10, rem = i & 1023, m = rem & 127, j8 = rem >> 7;
+                        const uint32_t sw = static_cast<uint32_t>(m & 7);
+                        const uint32_t c0 = 2u * static_cast<uint32_t>(j8 & 3);
+                        const uint32_t row = src0 + static_cast<uint32_t>((a * 2 + (j8 >> 2)) * kATileBytes + m * 128);
+                        float4 v0, v1;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(v0.x), "=f"(v0.y), "=f"(v0.z), "=f"(v0.w) : "r"(row + ((c0 ^ sw) << 4)));
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(v1.x), "=f"(v1.y), "=f"(v1.z), "=f"(v1.w) : "r"(row + (((c0 + 1) ^ sw) << 4)));
+                        st_shared_v4_u32(dst0 + static_cast<uint32_t>(a * kATileBytes + m * 128) +
+                                             ((static_cast<uint32_t>(j8) ^ sw) << 4),
+                                         pack_bf16x2(v0.x, v0.y), pack_bf16x2(v0.z, v0.w),
+                                         pack_bf16x2(v1.x, v1.y), pack_bf16x2(v1.z, v1.w));
+                    }
+                    if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
+                }
                 if constexpr (X3) {
                     // A_lo = A - trunc_tf32(A) (exact), elementwise over this CTA's A tile: the A tile
                     // and A_lo share the SW128 layout, so the copy is layout-agnostic
@@ -333,8 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool x3, bool olo) {
-    return make_layout(nacc, npad / cg, a_stages, o_stages, x3, olo).total + 1024;
+size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa, bool olo,
+                              int ks) {
+    return make_layout(nacc, npad / cg, a_stages, o_stages, xa, olo, ks).total + 1024;
 }
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
@@ -370,6 +418,10 @@ static cudaError_t dispatch_mode(const CUtensorMap& tmA, const SketchGemmParams&
         return launch_one<CG, NACC, DIST, kTF32, false>(tmA, p, grid, smem, s);
     }
     if (mode == kTF32x3) return launch_one<CG, NACC, DIST, kTF32x3, false>(tmA, p, grid, smem, s);
+    if (mode == kBF16) {
+        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kBF16, true>(tmA, p, grid, smem, s);
+        return launch_one<CG, NACC, DIST, kBF16, false>(tmA, p, grid, smem, s);
+    }
     return cudaErrorNotSupported;
 }
 
