@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -28,6 +29,7 @@ struct sk_sketch_s {
     int split_override;
     int cg_override;  // 0 auto, 1 force single-CTA tiles (ablation / tests)
     int core_simt;    // 1: force the fp32 SIMT core GEMM (tests / ablation)
+    int cl_override;  // 0 auto, 1 never share Omega between CTA pairs, 2 share whenever possible
     uint32_t ablate;  // performance ablations (bench only): see SketchGemmParams::ablate
     int profiling;
     std::mutex prof_mu;
@@ -113,6 +115,7 @@ struct SketchPlan {
     int npass;         // column passes of <= 256 columns
     int npad[32];      // MMA N per pass
     int cg;            // 1: one CTA per tile; 2: CTA pair (tcgen05 cta_group::2, M = 256)
+    int cl;            // 2: clusters of two CTA pairs sharing every generated Omega slice
     int nacc;
     int a_stages, o_stages;
     int split;
@@ -147,6 +150,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
         const int otile = (npad_max / P.cg) * 128;
         return (xa ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
     };
+    if (const char* e = getenv("SK_O_STAGES")) P.o_stages = std::max(1, std::min(8, atoi(e)));  // tuning
     for (;;) {
         const int a_stage = P.nacc * 128 * ks * 4;
         P.a_stages = std::min(6, (budget - P.o_stages * ostage_bytes(P.nacc)) / a_stage);
@@ -156,10 +160,24 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int a_stage = P.nacc * 128 * ks * 4;
     P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, xa, olo, ks);
     P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
-    const int rows_per_unit = 128 * P.cg * P.nacc;
+    // Clusters of two CTA pairs share each generated Omega slice (1024 rows of A per element).
+    // Automatic only in bf16 mode, whose 64-wide K steps amortise the extra cross-pair handshake
+    // (measured at c2: bf16 3.07 -> 2.29 ms; tf32 / tf32x3 with 32-wide steps were not faster);
+    // sketch_set_cta_group(h, 4) forces it in any mode.
+    const bool want_cl = (h->cl_override == 2) || (h->cl_override == 0 && bf);
+    P.cl = (want_cl && P.cg == 2 && P.nacc == 2 && n1 >= 2048 && npad_max % 32 == 0 &&
+            h->dist == sk::kGaussian) ? 2 : 1;
+    int workers = sk::num_sms() / P.cg;
+    if (P.cl == 2) {
+        const int mc = sk::sketch_gemm_max_clusters(P.cg, P.nacc, h->dist, h->mode,
+                                                    h->omega_transform == SK_OMEGA_FAST, P.cl, P.smem);
+        if (mc <= 0) P.cl = 1;
+        else workers = std::min(mc, sk::num_sms() / 4);
+    }
+    const int rows_per_unit = 128 * P.cg * P.nacc * P.cl;
     P.num_mblk = static_cast<int>((n1 + rows_per_unit - 1) / rows_per_unit);
     P.ws_per_split = static_cast<size_t>(n1) * npad_max * sizeof(float);
-    const int nsm = sk::num_sms() / P.cg;  // independent workers (CTAs or CTA pairs)
+    const int nsm = workers;  // independent workers (CTAs, CTA pairs or clusters of pairs)
     // The tensor core accumulates fp32 in TMEM with a bias toward zero of ~2^-24 per K=8 MMA step
     // (measured: relF = 7e-9 x K per accumulator, tools/acc_test.py).  tf32x3 promises fp32
     // accuracy (1e-5), so it caps K per accumulator at 1024 (32 K-iterations) with split-K; the
@@ -190,7 +208,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int kper = (P.kiters + best_s - 1) / best_s;
     P.split = (P.kiters + kper - 1) / kper;
     const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
-    P.grid = static_cast<int>(std::min<int64_t>(units, nsm)) * P.cg;
+    P.grid = static_cast<int>(std::min<int64_t>(units, nsm)) * P.cg * P.cl;
     if ((h->ablate & 8u) && (P.grid & 1)) P.grid += 1;  // cluster-of-2 ablation needs an even grid
     return P;
 }
@@ -300,7 +318,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         {
             LaunchScope ls(h, SK_PHASE_SKETCH_GEMM, stream);
             e = sk::launch_sketch_gemm(map, p, P.cg, P.nacc, h->dist, h->mode,
-                                       h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream);
+                                       h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream, P.cl);
         }
         if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
         if (P.split > 1) {
@@ -410,6 +428,7 @@ sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, 
     h->split_override = 0;
     h->cg_override = 0;
     h->core_simt = 0;
+    h->cl_override = 0;
     h->ablate = 0;
     h->profiling = 0;
     *out = h;
@@ -480,8 +499,9 @@ sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k) {
 
 sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    if (cg < 0 || cg > 2) return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1 or 2");
-    h->cg_override = cg;
+    if (cg < 0 || cg > 4 || cg == 3) return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1, 2 or 4");
+    h->cg_override = (cg == 4) ? 0 : cg;               // 4: pairs + cluster sharing
+    h->cl_override = (cg == 2) ? 1 : (cg == 4) ? 2 : 0;  // 2: pairs without cluster sharing
     return SK_SUCCESS;
 }
 

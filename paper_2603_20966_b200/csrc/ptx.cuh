@@ -302,3 +302,16 @@ __device__ __forceinline__ void st_shared_v4_u32(uint32_t addr, uint32_t a, uint
                  : "memory");
 }
 }  // namespace sk
+
+namespace sk {
+// Bulk copy shared::cta -> shared::cluster (another CTA of the cluster), completion counted in
+// bytes on the destination CTA's mbarrier (both given as shared::cluster addresses).
+__device__ __forceinline__ void bulk_copy_to_cta(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                                 uint32_t dst_bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst_cluster),
+        "r"(src_cta), "r"(bytes), "r"(dst_bar_cluster)
+        : "memory");
+}
+}  // namespace sk

@@ -53,13 +53,19 @@ __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stag
     L.a_off = 0;
     L.o_off = L.a_off + L.a_stage * a_stages;
     L.bar_off = L.o_off + L.o_stage * o_stages;
-    L.total = L.bar_off + (4 * kMaxStages + 4) * 8 + 16;
+    L.total = L.bar_off + (6 * kMaxStages + 4) * 8 + 16;
     return L;
 }
 
-template <int CG, int NACC, int DIST, int MODE, bool FAST>
+// CL = 2 (with CG = 2): a cluster of 4 CTAs = 2 CTA pairs processing different rows of A in
+// lockstep over the same K steps.  CTA (pair q, half h) needs the same Omega slice as its partner
+// (pair 1-q, half h); each generates half of the slice's rows and a copier thread bulk-copies that
+// half into the partner's stage (completing on the partner's full_o), so every generated Omega
+// element feeds 1024 rows of A.  The partner pair's MMA commit multicasts "stage free" (pfree).
+template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
+    static_assert(CL == 1 || CG == 2, "Omega sharing between pairs needs CTA pairs");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -79,16 +85,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty_a = bars + kMaxStages;
     uint64_t* full_o = bars + 2 * kMaxStages;
     uint64_t* empty_o = bars + 3 * kMaxStages;
-    uint64_t* tmem_full = bars + 4 * kMaxStages;
+    uint64_t* gen_done = bars + 4 * kMaxStages;  // CL = 2: this CTA's Omega half (+ A transform) written
+    uint64_t* pfree = bars + 5 * kMaxStages;     // CL = 2: the partner's stage s is free
+    uint64_t* tmem_full = bars + 6 * kMaxStages;
     uint64_t* tmem_empty = tmem_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 2);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0u;
+    const uint32_t crank_cl = (CG == 2) ? cluster_ctarank() : 0u;  // rank in the cluster
+    const uint32_t crank = crank_cl & 1u;                             // rank in the CTA pair
+    const uint32_t lead_rank = crank_cl & ~1u;                        // pair leader's cluster rank
+    const uint32_t pairq = crank_cl >> 1;                             // pair index in the cluster
+    const uint32_t partner = crank_cl ^ 2u;                           // CL = 2: same half, other pair
+    const uint16_t pair_mask = static_cast<uint16_t>(0x3u << lead_rank);
+    const uint16_t partner_pair_mask = static_cast<uint16_t>(0x3u << (lead_rank ^ 2u));
     const bool leader = crank == 0;
-    const int group = static_cast<int>(blockIdx.x) / CG;
-    const int ngroups = static_cast<int>(gridDim.x) / CG;
+    const int group = static_cast<int>(blockIdx.x) / (CG * CL);      // worker = pair (or cluster)
+    const int ngroups = static_cast<int>(gridDim.x) / (CG * CL);
     uint32_t tmem_cols = 32;
     while (tmem_cols < static_cast<uint32_t>(NACC * p.npad)) tmem_cols <<= 1;
 
@@ -102,10 +116,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&empty_a[s], 1);
         }
         for (int s = 0; s < p.o_stages; ++s) {
-            // leader: its own kRngWarps warps + (CG = 2) one relayed arrival for the peer's half;
-            // peer: its own kRngWarps warps (forwarded by the relay thread, warp 3)
-            mbar_init(&full_o[s], kRngWarps + ((CG == 2 && leader) ? 1 : 0));
+            // CL = 1: own kRngWarps warps; CL = 2: the copier's expect_tx arrival (after gen_done),
+            // plus the partner's bulk-copied half as tx bytes.  Leader: + the peer's relayed arrival.
+            mbar_init(&full_o[s], (CL == 2 ? 1 : kRngWarps) + ((CG == 2 && leader) ? 1 : 0));
             mbar_init(&empty_o[s], 1);
+            mbar_init(&gen_done[s], kRngWarps);
+            mbar_init(&pfree[s], 1);
         }
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, 4 * CG);
@@ -122,7 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int total_units = p.num_mblk * p.split;
-    const int rows_per_unit = 128 * CG * NACC;
+    const int rows_per_unit = 128 * CG * NACC * CL;   // rows of a work unit (all pairs of a cluster)
+    const int pair_row0 = static_cast<int>(pairq) * 128 * CG * NACC;  // this pair's rows inside a unit
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer
@@ -137,18 +154,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty_a[st], ph ^ 1);
                     const int x = kit * KS - p.kshift;
                     if (p.ablate & 2u) {  // ablation: no A traffic, stage marked full at once
-                        if (leader) mbar_arrive(&full_a[st]);
+                        if (leader || ARELAY) mbar_arrive(&full_a[st]);
                         if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
                         continue;
                     }
                     if constexpr (CG == 2 && !ARELAY) {
                         // both CTAs load their own rows; bytes are counted on the leader's barrier
-                        const uint32_t bar = mapa_shared(smem_u32(&full_a[st]), 0);
+                        const uint32_t bar = mapa_shared(smem_u32(&full_a[st]), lead_rank);
                         if (leader) mbar_arrive_expect_tx(&full_a[st], 2 * a_bytes_cta);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a)
                             tma_load_2d_pair(sA + st * L.a_stage + a * kATileBytes * NBOX, &tmA, bar, x,
-                                             mb * rows_per_unit + a * 256 + static_cast<int>(crank) * 128, pol);
+                                             mb * rows_per_unit + pair_row0 + a * 256 + static_cast<int>(crank) * 128, pol);
                     } else {
                         mbar_arrive_expect_tx(&full_a[st], a_bytes_cta);
 #pragma unroll
@@ -156,15 +173,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int bx = 0; bx < NBOX; ++bx)
                                 tma_load_2d(sA + st * L.a_stage + (a * NBOX + bx) * kATileBytes, &tmA, &full_a[st],
-                                            x + 32 * bx, mb * rows_per_unit + a * 128 * CG + static_cast<int>(crank) * 128, pol);
+                                            x + 32 * bx, mb * rows_per_unit + pair_row0 + a * 128 * CG +
+                                                             static_cast<int>(crank) * 128, pol);
                     }
                     if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && leader) {
         // ------------------------------------------------------------------ MMA issuer (leader)
-        if (leader && elect_one()) {
+        if (elect_one()) {
             const uint32_t idesc = make_idesc(BF ? kFmtBF16 : kFmtTF32, 128 * CG, static_cast<uint32_t>(p.npad), 0, 0);
             uint32_t sa = 0, pa = 0, so = 0, po = 0, local = 0;
             for (int u = group; u < total_units; u += ngroups, ++local) {
@@ -210,8 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                     if constexpr (CG == 2) {
-                        mma_commit_pair(&empty_a[sa], 0x3);
-                        mma_commit_pair(&empty_o[so], 0x3);
+                        mma_commit_pair(&empty_a[sa], pair_mask);
+                        mma_commit_pair(&empty_o[so], pair_mask);
+                        if constexpr (CL == 2) mma_commit_pair(&pfree[so], partner_pair_mask);
                     } else {
                         mma_commit(&empty_a[sa]);
                         mma_commit(&empty_o[so]);
@@ -219,26 +238,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                     if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
                 }
-                if constexpr (CG == 2) mma_commit_pair(tmem_full, 0x3);
+                if constexpr (CG == 2) mma_commit_pair(tmem_full, pair_mask);
                 else mma_commit(tmem_full);
             }
         }
-    } else if (warp == 2 || warp == 3) {
-        // ------------------------------------------------------------------ relays (peer CTA)
-        // The peer's producer warps arrive on its LOCAL full_o (cheap, CTA scope); one thread
-        // (warp 2) forwards a single release.cluster arrive per stage to the leader's full_o,
-        // keeping the cluster-scope fence off the producers' critical path.
-        if (CG == 2 && !leader && (warp == 2 || ARELAY) && elect_one()) {
-            uint64_t* bars_r = (warp == 2) ? full_o : full_a;  // warp 3 relays A (tf32x3 pairs)
-            const uint32_t nst = static_cast<uint32_t>((warp == 2) ? p.o_stages : p.a_stages);
+    } else if (warp == 2 || warp == 3 || (warp == 1 && !leader)) {
+        // ------------------------------------------------------------------ relays / copier
+        // Peer CTA: warp 2 forwards its full_o and (XA modes) warp 3 its full_a to the pair leader
+        // with a RELAXED cluster-scope arrive (a release.cluster arrive drains in-flight TMA
+        // traffic; the relay writes nothing itself).  CL = 2: the copier (leader: warp 3, peer:
+        // warp 1) pushes this CTA's Omega half into the partner pair's CTA.
+        const bool is_copier = (CL == 2) && ((leader && warp == 3) || (!leader && warp == 1));
+        const bool is_orelay = (CG == 2) && !leader && warp == 2;
+        const bool is_arelay = ARELAY && !leader && warp == 3;
+        if ((is_copier || is_orelay || is_arelay) && elect_one()) {
+            uint64_t* bars_r = is_orelay ? full_o : full_a;
+            const uint32_t nst = static_cast<uint32_t>(is_arelay ? p.a_stages : p.o_stages);
+            const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / 2);
+            const uint32_t half_bytes = gen_rows * 128u;
+            const uint32_t half_off = pairq * half_bytes;
+            const uint32_t tx = half_bytes * (OLO ? 2u : 1u);
             uint32_t st = 0, ph = 0;
             for (int u = group; u < total_units; u += ngroups) {
                 const int s = u - (u / p.split) * p.split;
                 const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
                 for (int kit = kb; kit < ke; ++kit) {
-                    mbar_wait(&bars_r[st], ph);
-                    if (p.ablate & 16u) mbar_arrive_cluster(mapa_shared(smem_u32(&bars_r[st]), 0));
-                    else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&bars_r[st]), 0));
+                    if (is_copier) {
+                        mbar_wait(&gen_done[st], ph);
+                        mbar_arrive_expect_tx(&full_o[st], tx);  // local half done; partner half incoming
+                        mbar_wait(&pfree[st], ph ^ 1);
+                        const uint32_t src = smem_u32(sO + st * L.o_stage + L.ohi_off) + half_off;
+                        const uint32_t bar = mapa_shared(smem_u32(&full_o[st]), partner);
+                        bulk_copy_to_cta(mapa_shared(src, partner), src, half_bytes, bar);
+                        if constexpr (OLO) {
+                            const uint32_t src_lo = smem_u32(sO + st * L.o_stage + L.olo_off) + half_off;
+                            bulk_copy_to_cta(mapa_shared(src_lo, partner), src_lo, half_bytes, bar);
+                        }
+                    } else {
+                        mbar_wait(&bars_r[st], ph);
+                        if (p.ablate & 16u) mbar_arrive_cluster(mapa_shared(smem_u32(&bars_r[st]), lead_rank));
+                        else mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&bars_r[st]), lead_rank));
+                    }
                     if (++st == nst) { st = 0; ph ^= 1; }
                 }
             }
@@ -246,9 +286,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= kCtlWarps) {
         // ------------------------------------------------------------------ Omega producers + epilogue
         const int t = static_cast<int>(threadIdx.x) - kCtlWarps * 32;
-        const int n_start = t % npad_loc, j_start = t / npad_loc;
-        const int tq = kRngThreads / npad_loc, tr = kRngThreads % npad_loc;
-        const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc;
+        const int gen_rows = (CL == 2) ? npad_loc / 2 : npad_loc;              // rows this CTA generates
+        const int gen_row0 = (CL == 2) ? static_cast<int>(pairq) * gen_rows : 0; // first generated row
+        const int n_start = t % gen_rows, j_start = t / gen_rows;
+        const int tq = kRngThreads / gen_rows, tr = kRngThreads % gen_rows;
+        const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
         uint32_t so = 0, po = 0, sa = 0, pa = 0, local = 0;
         const uint32_t lo_off = L.olo_off - L.ohi_off;
         for (int u = group; u < total_units; u += ngroups, ++local) {
@@ -257,24 +299,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kit = kb; kit < ke; ++kit) {
                 mbar_wait(&empty_o[so], po ^ 1);
                 uint8_t* ostage = sO + so * L.o_stage;
+                uint8_t* otile = ostage + L.ohi_off + gen_row0 * 128;  // this CTA's generated rows
                 if (p.ablate & 1u) {
                     // ablation: stage marked full without generating Omega
                 } else if constexpr (BF) {
                     if constexpr (DIST == kRademacher)
-                        produce_omega_tile_bf16_r<DIST, FAST>(ostage + L.ohi_off, p.k0a + static_cast<int64_t>(kit) * KS,
-                                                              p.roff, npad_loc, c0_loc, p.key0, p.key1, t);
+                        produce_omega_tile_bf16_r<DIST, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                              p.roff, gen_rows, c0_loc, p.key0, p.key1, t);
                     else
-                        produce_omega_tile_bf16_g<DIST, FAST>(ostage + L.ohi_off, p.k0a + static_cast<int64_t>(kit) * KS,
-                                                              p.roff, npad_loc, c0_loc, p.key0, p.key1,
+                        produce_omega_tile_bf16_g<DIST, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                              p.roff, gen_rows, c0_loc, p.key0, p.key1,
                                                               n_start, j_start, tq, tr);
                 } else if constexpr (DIST == kRademacher)
-                    produce_omega_tile_r<DIST, MODE, FAST>(ostage + L.ohi_off,
-                                                           p.k0a + static_cast<int64_t>(kit) * 32,
-                                                           p.roff, npad_loc, c0_loc, p.key0, p.key1, t, lo_off);
+                    produce_omega_tile_r<DIST, MODE, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * 32,
+                                                           p.roff, gen_rows, c0_loc, p.key0, p.key1, t, lo_off);
                 else
-                    produce_omega_tile_g<DIST, MODE, FAST>(ostage + L.ohi_off,
-                                                           p.k0a + static_cast<int64_t>(kit) * 32,
-                                                           p.roff, npad_loc, c0_loc, p.key0, p.key1,
+                    produce_omega_tile_g<DIST, MODE, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * 32,
+                                                           p.roff, gen_rows, c0_loc, p.key0, p.key1,
                                                            n_start, j_start, tq, tr, lo_off);
                 if constexpr (BF) {
                     // A (two fp32 SW128 boxes of 32 K per accumulator) -> one bf16 SW128 tile of 64 K:
@@ -317,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&full_o[so]);
+                if (lane == 0) mbar_arrive(CL == 2 ? &gen_done[so] : &full_o[so]);
                 if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
             }
             if (t < 128) {
@@ -329,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
                 for (int a = 0; a < NACC; ++a) {
-                    const int row = mb * rows_per_unit + a * 128 * CG + static_cast<int>(crank) * 128 +
+                    const int row = mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128 +
                                     q * 32 + static_cast<int>(lane);
                     float* orow = out + static_cast<int64_t>(row) * p.ldo;
 #pragma unroll 1
@@ -364,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(tmem_empty), 0));
+                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(tmem_empty), lead_rank));
                     else mbar_arrive(tmem_empty);
                 }
             }
@@ -387,10 +428,40 @@ size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_st
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
 
-template <int CG, int NACC, int DIST, int MODE, bool FAST>
+// Clusters of `cluster` CTAs of this kernel that can be co-resident (GPC packing strands SMs for
+// clusters of 4).  Returns 0 if the query fails.
+int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cg * cl * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cg * cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const void* fn = nullptr;
+#define SK_FN(M, F) fn = reinterpret_cast<const void*>(sketch_gemm_kernel<2, 2, kGaussian, M, F, 2>)
+    if (cg == 2 && cl == 2 && nacc == 2 && dist == kGaussian) {
+        if (mode == kTF32) { if (fast) SK_FN(kTF32, true); else SK_FN(kTF32, false); }
+        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true); else SK_FN(kBF16, false); }
+        else SK_FN(kTF32x3, false);
+    }
+#undef SK_FN
+    if (!fn) return 0;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) return 0;
+    return n;
+}
+
+template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL>
 static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p, int grid,
                               size_t smem, cudaStream_t s) {
-    auto kern = sketch_gemm_kernel<CG, NACC, DIST, MODE, FAST>;
+    auto kern = sketch_gemm_kernel<CG, NACC, DIST, MODE, FAST, CL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -402,7 +473,7 @@ static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p,
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     // ablation bit 3: launch single-CTA tiles as clusters of 2 (isolates cluster placement effects)
-    attr[0].val.clusterDim.x = (CG == 1 && (p.ablate & 8u)) ? 2 : CG;
+    attr[0].val.clusterDim.x = (CG == 1 && (p.ablate & 8u)) ? 2 : CG * CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -410,32 +481,34 @@ static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p,
     return cudaLaunchKernelEx(&cfg, kern, tmA, p);
 }
 
-template <int CG, int NACC, int DIST>
+template <int CG, int NACC, int DIST, int CL = 1>
 static cudaError_t dispatch_mode(const CUtensorMap& tmA, const SketchGemmParams& p, int mode,
                                  bool fast, int grid, size_t smem, cudaStream_t s) {
     if (mode == kTF32) {
-        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kTF32, true>(tmA, p, grid, smem, s);
-        return launch_one<CG, NACC, DIST, kTF32, false>(tmA, p, grid, smem, s);
+        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kTF32, true, CL>(tmA, p, grid, smem, s);
+        return launch_one<CG, NACC, DIST, kTF32, false, CL>(tmA, p, grid, smem, s);
     }
-    if (mode == kTF32x3) return launch_one<CG, NACC, DIST, kTF32x3, false>(tmA, p, grid, smem, s);
+    if (mode == kTF32x3) return launch_one<CG, NACC, DIST, kTF32x3, false, CL>(tmA, p, grid, smem, s);
     if (mode == kBF16) {
-        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kBF16, true>(tmA, p, grid, smem, s);
-        return launch_one<CG, NACC, DIST, kBF16, false>(tmA, p, grid, smem, s);
+        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kBF16, true, CL>(tmA, p, grid, smem, s);
+        return launch_one<CG, NACC, DIST, kBF16, false, CL>(tmA, p, grid, smem, s);
     }
     return cudaErrorNotSupported;
 }
 
-template <int CG, int NACC>
+template <int CG, int NACC, int CL = 1>
 static cudaError_t dispatch_dist(const CUtensorMap& tmA, const SketchGemmParams& p, int dist,
                                  int mode, bool fast, int grid, size_t smem, cudaStream_t s) {
-    if (dist == kGaussian) return dispatch_mode<CG, NACC, kGaussian>(tmA, p, mode, fast, grid, smem, s);
-    if (dist == kRademacher) return dispatch_mode<CG, NACC, kRademacher>(tmA, p, mode, fast, grid, smem, s);
-    return dispatch_mode<CG, NACC, kUniform>(tmA, p, mode, fast, grid, smem, s);
+    if (dist == kGaussian) return dispatch_mode<CG, NACC, kGaussian, CL>(tmA, p, mode, fast, grid, smem, s);
+    if (dist == kRademacher) return dispatch_mode<CG, NACC, kRademacher, CL>(tmA, p, mode, fast, grid, smem, s);
+    return dispatch_mode<CG, NACC, kUniform, CL>(tmA, p, mode, fast, grid, smem, s);
 }
 
 cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg, int nacc,
                                int dist, int mode, bool fast, int grid, size_t smem,
-                               cudaStream_t s) {
+                               cudaStream_t s, int cl) {
+    if (cl == 2 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 2>(tmA, p, dist, mode, fast, grid, smem, s);
+    if (cl == 2 && cg == 2 && nacc == 1) return dispatch_dist<2, 1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cg == 1 && nacc == 1) return dispatch_dist<1, 1>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cg == 1 && nacc == 2) return dispatch_dist<1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cg == 2 && nacc == 1) return dispatch_dist<2, 1>(tmA, p, dist, mode, fast, grid, smem, s);

@@ -256,10 +256,11 @@ def test_error_codes():
     assert s.apply(torch.zeros((0, 100), device="cuda")).shape == (0, 8)
 
 
-@pytest.mark.parametrize("cg", [1, 2])
-@pytest.mark.parametrize("shape", [(1000, 3000, 256), (600, 1000, 48), (2049, 700, 128)])
+@pytest.mark.parametrize("cg", [1, 2, 4])
+@pytest.mark.parametrize("shape", [(1000, 3000, 256), (600, 1000, 48), (2049, 700, 128), (5000, 2000, 256)])
 def test_cta_group_variants(cg, shape):
-    """Single-CTA tiles and CTA pairs (tcgen05 cta_group::2) agree with the oracle in every mode."""
+    """Single-CTA tiles, CTA pairs (tcgen05 cta_group::2) and clusters of two pairs sharing the
+    generated Omega slices (cg=4, n1 >= 2048) agree with the oracle in every mode."""
     sk = _sk()
     n1, n2, r = shape
     Ai = synth.int_matrix(11, n1, n2, -4, 4)
@@ -291,3 +292,19 @@ def test_fast_transform_rejected_in_tf32x3():
     with pytest.raises(sk.SketchError) as e:
         s.apply(torch.zeros((4, 100), device="cuda"))
     assert e.value.name == "SK_ERR_UNSUPPORTED"
+
+
+@pytest.mark.parametrize("mode", ["tf32", "bf16", "tf32x3"])
+@pytest.mark.parametrize("omega", ["accurate", "fast"])
+def test_cluster_sharing_bit_identical(mode, omega):
+    """Sharing generated Omega halves between two CTA pairs changes which SM computes a row, not
+    the MMA sequence a row sees: B must equal the unshared CTA-pair result bit for bit."""
+    if mode == "tf32x3" and omega == "fast":
+        pytest.skip("fast transform not allowed in tf32x3")
+    sk = _sk()
+    A = _dev(synth.uniform(21, 4100, 3000))
+    outs = []
+    for cg in (2, 4):
+        s = sk.Sketch(SEED, "gaussian", 3000, 256, mode=mode, omega=omega, cta_group=cg, split_k=3)
+        outs.append(s.apply(A))
+    assert torch.equal(outs[0], outs[1])
