@@ -305,8 +305,10 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h0 = time.perf_counter()
     for _ in range(args.steps):
         out = step()
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host submission time per step
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -354,7 +356,7 @@ def main():
         "traffic": None,
     })
     prof_path = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{args.mode}_{args.omega}.json")
-    if os.path.exists(prof_path):
+    if os.path.exists(prof_path) and world == 1:  # the capture is of the 1-GPU launch
         with open(prof_path) as f:
             tr = json.load(f)
         roof["traffic"] = tr.get("dram_bytes_per_launch")
@@ -373,6 +375,7 @@ def main():
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
         "roofline": roof,
         "gpu_launches": launches,
+        "host_submit_ms_per_step": host_ms,
         "clocks": clocks,
         "comm": {"predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"]),
                  "measured_bytes_per_rank": comm_bytes},

@@ -192,14 +192,17 @@ class Sketch:
         return int(n.value)
 
     def workspace(self, n1: int, device=None):
+        """Device workspace for n1 rows (cached per (device, n1): no ABI query on the hot path)."""
         torch = _torch()
-        nbytes = self.workspace_size(n1)
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        key = (dev.index, nbytes)
+        key = (dev.index, int(n1))
         ws = self._ws.get(key)
         if ws is None:
+            nbytes = self.workspace_size(n1)
             ws = torch.empty(max(nbytes, 16) // 4 + 4, dtype=torch.float32, device=dev)
-            self._ws = {key: ws}
+            if len(self._ws) > 8:
+                self._ws.clear()
+            self._ws[key] = ws
         return ws
 
     # ------------------------------------------------------------------ hot path

@@ -34,7 +34,22 @@ struct sk_sketch_s {
     int profiling;
     std::mutex prof_mu;
     std::vector<sk_timed_launch> prof;
+    std::vector<cudaEvent_t> event_pool;  // reused by LaunchScope (no create/destroy per launch)
 };
+
+static cudaEvent_t pool_get(sk_sketch_s* h) {
+    {
+        std::lock_guard<std::mutex> g(h->prof_mu);
+        if (!h->event_pool.empty()) {
+            cudaEvent_t e = h->event_pool.back();
+            h->event_pool.pop_back();
+            return e;
+        }
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
 
 static std::atomic<uint64_t> g_launches{0};
 
@@ -47,8 +62,8 @@ struct LaunchScope {
     LaunchScope(sk_sketch_s* h_, int phase_, cudaStream_t s_) : h(h_), phase(phase_), s(s_) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (h && h->profiling) {
-            cudaEventCreate(&e0);
-            cudaEventCreate(&e1);
+            e0 = pool_get(h);
+            e1 = pool_get(h);
             cudaEventRecord(e0, s);
         }
     }
@@ -351,10 +366,19 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         q.nchunks = CP.chunks;
         q.key0 = static_cast<uint32_t>(h->seed);
         q.key1 = static_cast<uint32_t>(h->seed >> 32);
+        // partials [nchunks * r, r] stored by TMA in 32x32 tiles when r is a multiple of 32
+        CUtensorMap omap;
+        q.tma_store = (h->r % 32 == 0 && aligned16(ws)) ? 1 : 0;
+        if (q.tma_store) {
+            if (sk_status_t st = make_map_2d(&omap, q.part, static_cast<int64_t>(q.nchunks) * h->r, h->r, h->r, 32, 32))
+                return st;
+        } else {
+            omap = map;  // unused
+        }
         cudaError_t e;
         {
             LaunchScope ls(h, SK_PHASE_CORE_GEMM, stream);
-            e = sk::launch_core_gemm_tc(map, q, CP.nacc, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
+            e = sk::launch_core_gemm_tc(map, omap, q, CP.nacc, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "core_gemm_tc launch");
         {
@@ -438,6 +462,7 @@ sk_status_t sketch_create(uint64_t seed, sk_dist_t dist, int64_t n2, int64_t r, 
 sk_status_t sketch_destroy(sk_sketch_t h) {
     if (h) {
         for (auto& t : h->prof) { cudaEventDestroy(t.start); cudaEventDestroy(t.end); }
+        for (auto e : h->event_pool) cudaEventDestroy(e);
         delete h;
     }
     return SK_SUCCESS;
@@ -466,8 +491,13 @@ sk_status_t sketch_profile_read(sk_sketch_t h, double* ms, int64_t* launches) {
         if (err != cudaSuccess && st == SK_SUCCESS) st = cuda_fail(err, "profile event");
         ms[t.phase] += e;
         launches[t.phase] += 1;
-        cudaEventDestroy(t.start);
-        cudaEventDestroy(t.end);
+    }
+    {
+        std::lock_guard<std::mutex> g(h->prof_mu);
+        for (auto& t : v) {
+            h->event_pool.push_back(t.start);
+            h->event_pool.push_back(t.end);
+        }
     }
     return st;
 }

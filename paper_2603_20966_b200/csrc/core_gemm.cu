@@ -136,7 +136,7 @@ constexpr int kCoreStages = 2;     // operand (Omega^T + B^T) ring
 constexpr int kCoreRawStages = 2;  // raw B ring (TMA)
 
 struct CoreSmem {
-    uint32_t raw_stage, o_stage, bt_stage, raw_off, o_off, bt_off, bar_off, total;
+    uint32_t raw_stage, o_stage, bt_stage, raw_off, o_off, bt_off, epi_off, bar_off, total;
 };
 __host__ __device__ inline CoreSmem core_smem(int nacc, int npad) {
     CoreSmem L;
@@ -146,14 +146,16 @@ __host__ __device__ inline CoreSmem core_smem(int nacc, int npad) {
     L.raw_off = 0;
     L.o_off = L.raw_off + kCoreRawStages * L.raw_stage;
     L.bt_off = L.o_off + kCoreStages * L.o_stage;
-    L.bar_off = L.bt_off + kCoreStages * L.bt_stage;
+    L.epi_off = L.bt_off + kCoreStages * L.bt_stage;  // 4 warps x 2 x 4 KB TMA-store staging
+    L.bar_off = L.epi_off + 4 * 8192;
     L.total = L.bar_off + (2 * kCoreRawStages + 2 * kCoreStages + 2) * 8 + 16;
     return L;
 }
 
 template <int NACC, int DIST, int MODE, bool FAST>
 __global__ void __launch_bounds__(kCoreThreads, 1)
-    core_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const CoreTcParams p) {
+    core_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmOut,
+                        const CoreTcParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -272,10 +274,13 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             mbar_wait(done, 0);
             tc_fence_after();
             float* out = p.part + static_cast<int64_t>(chunk) * p.r * p.ldp;
+            uint8_t* epi = smem + L.epi_off + q * 8192;
+            int ebuf = 0;
 #pragma unroll 1
             for (int a = 0; a < NACC; ++a) {
                 const int row = a * 128 + q * 32 + static_cast<int>(lane);  // Omega column a
                 float* orow = out + static_cast<int64_t>(row) * p.ldp;
+                if (p.tma_store && a * 128 + q * 32 >= p.r) continue;  // padding rows of the last block
 #pragma unroll 1
                 for (int cc = 0; cc < p.npad; cc += 32) {
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -290,13 +295,16 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
                         for (int i = 0; i < 16; ++i) { v[i] = h[i]; v[16 + i] = 0u; }
                     }
                     tmem_ld_wait();
-                    if (row < p.r) {
+                    if (p.tma_store) {
+                        epi_store_tile(&tmOut, epi, ebuf, v, cc, chunk * p.r + a * 128 + q * 32);
+                    } else if (row < p.r) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
                             if (cc + i < p.r) orow[cc + i] = __uint_as_float(v[i]);
                     }
                 }
             }
+            if (p.tma_store && lane == 0) bulk_wait_group<0>();
         }
     }
     tc_fence_before();
@@ -310,28 +318,33 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
 size_t core_gemm_tc_smem_bytes(int nacc, int npad) { return core_smem(nacc, npad).total + 1024; }
 
 template <int NACC, int DIST, int MODE, bool FAST>
-static cudaError_t launch_core_tc_one(const CUtensorMap& tmB, const CoreTcParams& p, cudaStream_t s) {
+static cudaError_t launch_core_tc_one(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
+                                      cudaStream_t s) {
     auto kern = core_gemm_tc_kernel<NACC, DIST, MODE, FAST>;
     const size_t smem = core_gemm_tc_smem_bytes(NACC, p.npad);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    kern<<<p.nchunks, kCoreThreads, smem, s>>>(tmB, p);
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
+    kern<<<p.nchunks, kCoreThreads, smem, s>>>(tmB, tmOut, p);
     return cudaGetLastError();
 }
 
 template <int NACC>
-static cudaError_t core_tc_dist(const CUtensorMap& tmB, const CoreTcParams& p, int dist, bool fast,
-                                cudaStream_t s) {
-    if (dist == kRademacher) return launch_core_tc_one<NACC, kRademacher, kTF32, false>(tmB, p, s);
-    if (dist == kUniform) return launch_core_tc_one<NACC, kUniform, kTF32, false>(tmB, p, s);
-    if (fast) return launch_core_tc_one<NACC, kGaussian, kTF32, true>(tmB, p, s);
-    return launch_core_tc_one<NACC, kGaussian, kTF32, false>(tmB, p, s);
+static cudaError_t core_tc_dist(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
+                                int dist, bool fast, cudaStream_t s) {
+    if (dist == kRademacher) return launch_core_tc_one<NACC, kRademacher, kTF32, false>(tmB, tmOut, p, s);
+    if (dist == kUniform) return launch_core_tc_one<NACC, kUniform, kTF32, false>(tmB, tmOut, p, s);
+    if (fast) return launch_core_tc_one<NACC, kGaussian, kTF32, true>(tmB, tmOut, p, s);
+    return launch_core_tc_one<NACC, kGaussian, kTF32, false>(tmB, tmOut, p, s);
 }
 
-cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CoreTcParams& p, int nacc, int dist,
-                                bool fast, cudaStream_t s) {
-    if (nacc == 1) return core_tc_dist<1>(tmB, p, dist, fast, s);
-    if (nacc == 2) return core_tc_dist<2>(tmB, p, dist, fast, s);
+cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
+                                int nacc, int dist, bool fast, cudaStream_t s) {
+    if (nacc == 1) return core_tc_dist<1>(tmB, tmOut, p, dist, fast, s);
+    if (nacc == 2) return core_tc_dist<2>(tmB, tmOut, p, dist, fast, s);
     return cudaErrorNotSupported;
 }
 

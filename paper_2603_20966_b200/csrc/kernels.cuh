@@ -58,6 +58,7 @@ struct CoreTcParams {
     int32_t r;
     int32_t npad;         // MMA N (multiple of 16, <= 256)
     int32_t nchunks;
+    int32_t tma_store;    // 1: epilogue stores 32x32 tiles with TMA through tmOut (r % 32 == 0)
     uint32_t key0, key1;
 };
 
@@ -84,8 +85,8 @@ cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t
                                  int64_t ldo, cudaStream_t s);
 
 cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaStream_t s);
-cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CoreTcParams& p, int nacc, int dist,
-                                bool fast, cudaStream_t s);
+cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
+                                int nacc, int dist, bool fast, cudaStream_t s);
 size_t core_gemm_tc_smem_bytes(int nacc, int npad);
 cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
                                int64_t ldc, cudaStream_t s);

@@ -315,3 +315,49 @@ __device__ __forceinline__ void bulk_copy_to_cta(uint32_t dst_cluster, uint32_t 
         : "memory");
 }
 }  // namespace sk
+
+namespace sk {
+// TMA 2D store shared::cta -> global (bulk async group of the issuing thread).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups of this thread still READ their shared source
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Epilogue helper: one warp owns 32 TMEM lanes (= 32 output rows); moves a 32 x 32 fp32 tile from
+// registers (thread i = row i, v[0..31] = columns) into a SWIZZLE_128B staging tile (4 KB) and
+// TMA-stores it to (x, y) of `map`.  Double-buffered staging; lane 0 issues the bulk ops.
+__device__ __forceinline__ void epi_store_tile(const CUtensorMap* map, uint8_t* stage2, int& buf,
+                                               const uint32_t (&v)[32], int32_t x, int32_t y) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint8_t* st = stage2 + buf * 4096;
+    if (lane == 0) bulk_wait_group_read<1>();  // the store that used this buffer finished reading
+    __syncwarp();
+    const uint32_t base = smem_u32(st) + lane * 128u;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t addr = base + ((static_cast<uint32_t>(c) ^ (lane & 7u)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v[4 * c]),
+                     "r"(v[4 * c + 1]), "r"(v[4 * c + 2]), "r"(v[4 * c + 3])
+                     : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(map, st, x, y);
+        bulk_commit_group();
+    }
+    buf ^= 1;
+}
+}  // namespace sk

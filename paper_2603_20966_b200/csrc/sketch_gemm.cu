@@ -431,6 +431,8 @@ int sketch_gemm_max_smem() { return 227 * 1024; }
 // Clusters of `cluster` CTAs of this kernel that can be co-resident (GPC packing strands SMs for
 // clusters of 4).  Returns 0 if the query fails.
 int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem) {
+    static int cache[4][2] = {{-1, -1}, {-1, -1}, {-1, -1}, {-1, -1}};  // [mode][fast], per process
+    if (mode >= 0 && mode < 4 && cache[mode][fast ? 1 : 0] >= 0) return cache[mode][fast ? 1 : 0];
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cg * cl * 64);
     cfg.blockDim = dim3(kThreads);
@@ -455,6 +457,7 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return 0;
     if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) return 0;
+    if (mode >= 0 && mode < 4) cache[mode][fast ? 1 : 0] = n;
     return n;
 }
 
@@ -462,9 +465,13 @@ template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL>
 static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p, int grid,
                               size_t smem, cudaStream_t s) {
     auto kern = sketch_gemm_kernel<CG, NACC, DIST, MODE, FAST, CL>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    static size_t smem_set = 0;  // per instantiation: raise the opt-in smem limit once
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
