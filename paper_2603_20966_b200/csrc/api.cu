@@ -155,14 +155,15 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const bool x3 = h->mode == sk::kTF32x3;
     const bool bf = h->mode == sk::kBF16;
     const bool xa = x3 || bf;
-    const int ks = bf ? 64 : 32;
+    const bool t64 = (h->mode == sk::kTF32) && P.cg == 2;  // tf32 pairs run 64-wide K steps
+    const int ks = (bf || t64) ? 64 : 32;
+    const int nsubo = t64 ? 2 : 1;
     const bool olo = x3 && h->dist != sk::kRademacher;
-    // CTA pairs hand every Omega stage across the pair (relay + multicast commit): a deeper ring
-    // hides that round trip in the fast modes; tf32x3 stages are 2-3x larger and MMA-bound.
-    P.o_stages = xa ? 2 : ((P.cg == 2) ? 4 : 2);
+    // Omega ring depth: pairs hand every stage across the pair (relay + multicast commit)
+    P.o_stages = xa ? 2 : ((P.cg == 2) ? 3 : 2);
     const int budget = sk::sketch_gemm_max_smem() - 2048;
     auto ostage_bytes = [&](int nacc) {
-        const int otile = (npad_max / P.cg) * 128;
+        const int otile = (npad_max / P.cg) * 128 * nsubo;
         return (xa ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
     };
     if (const char* e = getenv("SK_O_STAGES")) P.o_stages = std::max(1, std::min(8, atoi(e)));  // tuning
@@ -170,10 +171,10 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
         const int a_stage = P.nacc * 128 * ks * 4;
         P.a_stages = std::min(6, (budget - P.o_stages * ostage_bytes(P.nacc)) / a_stage);
         if (P.a_stages >= 2 || P.nacc == 1) break;
-        P.nacc = 1;  // tf32x3 single-CTA tiles: make room for >= 2 A stages
+        P.nacc = 1;  // make room for >= 2 A stages
     }
     const int a_stage = P.nacc * 128 * ks * 4;
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, xa, olo, ks);
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, xa, olo, ks, nsubo);
     P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
     // Clusters of two CTA pairs share each generated Omega slice (1024 rows of A per element).
     // Automatic only in bf16 mode, whose 64-wide K steps amortise the extra cross-pair handshake

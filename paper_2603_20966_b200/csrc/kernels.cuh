@@ -77,7 +77,7 @@ cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p
                                cudaStream_t s, int cl = 1);
 int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem);
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa,
-                              bool olo, int ks);
+                              bool olo, int ks, int nsubo);
 int sketch_gemm_max_smem();
 
 cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,

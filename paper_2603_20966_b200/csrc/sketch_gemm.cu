@@ -42,10 +42,12 @@ struct SmemLayout {
 // xa: the producers write a transformed A operand tile (tf32x3: A_lo fp32; bf16: A in bf16), which
 // takes nacc * 16 KB in the operand stage in both cases.
 __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stages, int o_stages,
-                                                  bool xa = false, bool olo = false, int ks = 32) {
+                                                  bool xa = false, bool olo = false, int ks = 32,
+                                                  int nsubo = 1) {
     SmemLayout L;
     L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes * static_cast<uint32_t>(ks / 32);
-    const uint32_t otile = static_cast<uint32_t>(npad) * 128u;
+    // nsubo: 32-K sub-tiles per Omega stage (2 for tf32 with 64-wide K steps)
+    const uint32_t otile = static_cast<uint32_t>(npad) * 128u * static_cast<uint32_t>(nsubo);
     L.alo_off = 0;
     L.ohi_off = xa ? static_cast<uint32_t>(nacc) * kATileBytes : 0u;
     L.olo_off = L.ohi_off + otile;
@@ -74,10 +76,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr bool XA = X3 || BF;                          // producers transform A in smem
     constexpr bool OLO = X3 && (DIST != kRademacher);      // +-1 is exact in tf32: no Omega_lo
     constexpr bool ARELAY = (CG == 2) && XA;               // peer A lands on its own barrier
-    constexpr int KS = BF ? 64 : 32;                       // K per pipeline step
+    constexpr bool T64 = (MODE == kTF32) && (CG == 2);    // tf32 pairs: 64-wide K steps
+    constexpr int KS = (BF || T64) ? 64 : 32;              // K per pipeline step
     constexpr int NBOX = KS / 32;                          // 128-B TMA boxes per accumulator
+    constexpr int NSUBO = T64 ? 2 : 1;                     // 32-K Omega sub-tiles per stage
+    constexpr int KMMA = T64 ? 8 : 4;                      // MMAs (per accumulator) per stage
     const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
-    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, XA, OLO, KS);
+    const uint32_t osub = static_cast<uint32_t>(npad_loc) * 128u;  // bytes of one Omega sub-tile
+    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, XA, OLO, KS, NSUBO);
     uint8_t* sA = smem + L.a_off;
     uint8_t* sO = smem + L.o_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -164,8 +170,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (leader) mbar_arrive_expect_tx(&full_a[st], 2 * a_bytes_cta);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a)
-                            tma_load_2d_pair(sA + st * L.a_stage + a * kATileBytes * NBOX, &tmA, bar, x,
-                                             mb * rows_per_unit + pair_row0 + a * 256 + static_cast<int>(crank) * 128, pol);
+#pragma unroll
+                            for (int bx = 0; bx < NBOX; ++bx)
+                                tma_load_2d_pair(sA + st * L.a_stage + (a * NBOX + bx) * kATileBytes, &tmA, bar,
+                                                 x + 32 * bx,
+                                                 mb * rows_per_unit + pair_row0 + a * 256 + static_cast<int>(crank) * 128, pol);
                     } else {
                         mbar_arrive_expect_tx(&full_a[st], a_bytes_cta);
 #pragma unroll
@@ -197,11 +206,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t a_base = smem_u32(sA + sa * L.a_stage);
                     const uint32_t o_base = smem_u32(sO + so * L.o_stage);
 #pragma unroll
-                    for (int k8 = 0; k8 < ((p.ablate & 4u) ? 0 : 4); ++k8) {
-                        const uint64_t bdesc = sw128_desc(o_base + L.ohi_off + k8 * 32, 16, 1024);
+                    for (int k8 = 0; k8 < ((p.ablate & 4u) ? 0 : KMMA); ++k8) {
+                        const int sub = k8 >> 2, kk = k8 & 3;  // 32-K sub-tile, 8-K step inside it
+                        const uint64_t bdesc = sw128_desc(o_base + L.ohi_off + sub * osub + kk * 32, 16, 1024);
 #pragma unroll
                         for (int a = 0; a < NACC; ++a) {
-                            const uint64_t adesc = sw128_desc(a_base + a * kATileBytes + k8 * 32, 16, 1024);
+                            const uint64_t adesc = sw128_desc(a_base + (a * NBOX + sub) * kATileBytes + kk * 32, 16, 1024);
                             uint32_t acc = (kit > kb || k8 > 0) ? 1u : 0u;
                             const uint32_t d = tmem_base + a * p.npad;
                             if constexpr (X3) {
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / 2);
             const uint32_t half_bytes = gen_rows * 128u;
             const uint32_t half_off = pairq * half_bytes;
-            const uint32_t tx = half_bytes * (OLO ? 2u : 1u);
+            const uint32_t tx = half_bytes * (OLO ? 2u : 1u) * NSUBO;
             uint32_t st = 0, ph = 0;
             for (int u = group; u < total_units; u += ngroups) {
                 const int s = u - (u / p.split) * p.split;
@@ -267,9 +277,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&gen_done[st], ph);
                         mbar_arrive_expect_tx(&full_o[st], tx);  // local half done; partner half incoming
                         mbar_wait(&pfree[st], ph ^ 1);
-                        const uint32_t src = smem_u32(sO + st * L.o_stage + L.ohi_off) + half_off;
                         const uint32_t bar = mapa_shared(smem_u32(&full_o[st]), partner);
-                        bulk_copy_to_cta(mapa_shared(src, partner), src, half_bytes, bar);
+#pragma unroll
+                        for (int sb = 0; sb < NSUBO; ++sb) {
+                            const uint32_t src = smem_u32(sO + st * L.o_stage + L.ohi_off) + sb * osub + half_off;
+                            bulk_copy_to_cta(mapa_shared(src, partner), src, half_bytes, bar);
+                        }
                         if constexpr (OLO) {
                             const uint32_t src_lo = smem_u32(sO + st * L.o_stage + L.olo_off) + half_off;
                             bulk_copy_to_cta(mapa_shared(src_lo, partner), src_lo, half_bytes, bar);
@@ -311,12 +324,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                               p.roff, gen_rows, c0_loc, p.key0, p.key1,
                                                               n_start, j_start, tq, tr);
                 } else if constexpr (DIST == kRademacher)
-                    produce_omega_tile_r<DIST, MODE, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * 32,
-                                                           p.roff, gen_rows, c0_loc, p.key0, p.key1, t, lo_off);
+                    for (int sb = 0; sb < NSUBO; ++sb)
+                        produce_omega_tile_r<DIST, MODE, FAST>(otile + sb * osub,
+                                                               p.k0a + static_cast<int64_t>(kit) * KS + 32 * sb,
+                                                               p.roff, gen_rows, c0_loc, p.key0, p.key1, t, lo_off);
                 else
-                    produce_omega_tile_g<DIST, MODE, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * 32,
-                                                           p.roff, gen_rows, c0_loc, p.key0, p.key1,
-                                                           n_start, j_start, tq, tr, lo_off);
+                    for (int sb = 0; sb < NSUBO; ++sb)
+                        produce_omega_tile_g<DIST, MODE, FAST>(otile + sb * osub,
+                                                               p.k0a + static_cast<int64_t>(kit) * KS + 32 * sb,
+                                                               p.roff, gen_rows, c0_loc, p.key0, p.key1,
+                                                               n_start, j_start, tq, tr, lo_off);
                 if constexpr (BF) {
                     // A (two fp32 SW128 boxes of 32 K per accumulator) -> one bf16 SW128 tile of 64 K:
                     // item (acc a, row m, chunk j8 = 8 K-values); a warp covers 32 consecutive rows
@@ -422,8 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa, bool olo,
-                              int ks) {
-    return make_layout(nacc, npad / cg, a_stages, o_stages, xa, olo, ks).total + 1024;
+                              int ks, int nsubo) {
+    return make_layout(nacc, npad / cg, a_stages, o_stages, xa, olo, ks, nsubo).total + 1024;
 }
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
