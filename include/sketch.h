@@ -132,6 +132,25 @@ sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64
                              int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
                              void* stream);
 
+/* Host-buffer / out-of-core forms: A, B and C are HOST pointers (page-locked memory --
+ * cudaHostAlloc / cudaHostRegister -- gives full PCIe bandwidth; pageable memory works but the
+ * copies then serialise).  A is streamed in row blocks of `block_rows` rows through two device
+ * staging buffers carved from the caller's DEVICE workspace `ws`: the H2D copy of block i+1 runs on
+ * a library-internal copy stream while block i is sketched on `stream`, then B's block i is copied
+ * back.  Rows of B are independent (row-block case), so any A that fits in host
+ * memory can be sketched on one GPU.  nystrom_core_host additionally accumulates
+ * C = sum_blocks Omega_blk^T B_blk in fixed block order (deterministic).
+ * All work is enqueued on `stream` (the copy stream is joined back into it): synchronise `stream`
+ * before reading B / C.  block_rows <= 0 picks a default (8192).  ws_bytes >= the size reported by
+ * sketch_host_workspace_size(h, n1, block_rows).  Errors as for the device forms. */
+sk_status_t sketch_host_workspace_size(sk_sketch_t h, int64_t n1, int64_t block_rows, size_t* bytes);
+sk_status_t sketch_apply_host(sk_sketch_t h, const float* A_host, int64_t n1, int64_t n2, int64_t lda,
+                              float* B_host, int64_t ldb, int64_t block_rows, void* ws,
+                              size_t ws_bytes, void* stream);
+sk_status_t nystrom_core_host(sk_sketch_t h, const float* A_host, int64_t n, int64_t lda,
+                              float* B_host, int64_t ldb, float* C_host, int64_t ldc,
+                              int64_t block_rows, void* ws, size_t ws_bytes, void* stream);
+
 /* Test / debug: materialise Omega[row0 : row0+nrows, col0 : col0+ncols] (fp32, accurate transform)
  * or the raw Philox word each entry derives from (x[j&3] for tag 0, x[(j>>5)&3] for tag 1),
  * row-major into device memory `out` with leading dimension ld >= ncols.

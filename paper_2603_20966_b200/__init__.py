@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "sketch_generate", "sketch_generate_bits",
+    "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
 )
@@ -76,6 +77,9 @@ def load_library(build_if_missing: bool = True):
         lib.nystrom_core.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
         lib.sketch_apply_block.argtypes = [vp, vp, i64, i64, i64, i64, vp, i64, vp, sz, vp]
         lib.core_apply_block.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, sz, vp]
+        lib.sketch_host_workspace_size.argtypes = [vp, i64, i64, ctypes.POINTER(sz)]
+        lib.sketch_apply_host.argtypes = [vp, vp, i64, i64, i64, vp, i64, i64, vp, sz, vp]
+        lib.nystrom_core_host.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, i64, vp, sz, vp]
         lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_generate_bits.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_debug_box_muller.argtypes = [vp, vp, i64, ctypes.c_int, vp, vp, vp]
@@ -260,6 +264,56 @@ class Sketch:
         _check(self._lib.nystrom_core(self._h, A.data_ptr(), n, A.stride(0), B.data_ptr(), B.stride(0),
                                       C.data_ptr(), C.stride(0), ws.data_ptr(), ws.numel() * 4,
                                       _stream_ptr(stream)))
+        return B, C
+
+    # ------------------------------------------------------------------ host buffers / out-of-core
+    def _host_ws(self, n1: int, block_rows: int):
+        torch = _torch()
+        n = ctypes.c_size_t()
+        _check(self._lib.sketch_host_workspace_size(self._h, int(n1), int(block_rows), ctypes.byref(n)))
+        key = ("host", torch.cuda.current_device(), int(n1), int(block_rows))
+        ws = self._ws.get(key)
+        if ws is None:
+            ws = torch.empty(max(n.value, 16) // 4 + 4, dtype=torch.float32, device="cuda")
+            self._ws[key] = ws
+        return ws
+
+    def apply_host(self, A, out=None, block_rows: int = 0, stream=None, sync: bool = True):
+        """B = A Omega for a HOST (CPU) fp32 A, streamed through the GPU in row blocks.
+
+        Pin A (A.pin_memory()) for full PCIe bandwidth.  Returns a CPU tensor (pinned if out is None)."""
+        torch = _torch()
+        _require_cuda()
+        if A.is_cuda or A.dtype != torch.float32 or A.stride(1) != 1:
+            raise SketchError(1, "SK_ERR_INVALID_VALUE", "expected a row-major fp32 CPU tensor")
+        n1, n2 = A.shape
+        if out is None:
+            out = torch.empty((n1, self.r), dtype=torch.float32, pin_memory=True)
+        ws = self._host_ws(n1, block_rows)
+        _check(self._lib.sketch_apply_host(self._h, A.data_ptr(), n1, n2, A.stride(0), out.data_ptr(),
+                                           out.stride(0), int(block_rows), ws.data_ptr(), ws.numel() * 4,
+                                           _stream_ptr(stream)))
+        if sync:
+            (stream or torch.cuda.current_stream()).synchronize()
+        return out
+
+    def nystrom_core_host(self, A, B=None, C=None, block_rows: int = 0, stream=None, sync: bool = True):
+        """(B, C) for a HOST square A streamed in row blocks (out-of-core Nystrom core)."""
+        torch = _torch()
+        _require_cuda()
+        if A.is_cuda or A.dtype != torch.float32 or A.stride(1) != 1:
+            raise SketchError(1, "SK_ERR_INVALID_VALUE", "expected a row-major fp32 CPU tensor")
+        n = A.shape[0]
+        if B is None:
+            B = torch.empty((n, self.r), dtype=torch.float32, pin_memory=True)
+        if C is None:
+            C = torch.empty((self.r, self.r), dtype=torch.float32, pin_memory=True)
+        ws = self._host_ws(n, block_rows)
+        _check(self._lib.nystrom_core_host(self._h, A.data_ptr(), n, A.stride(0), B.data_ptr(), B.stride(0),
+                                           C.data_ptr(), C.stride(0), int(block_rows), ws.data_ptr(),
+                                           ws.numel() * 4, _stream_ptr(stream)))
+        if sync:
+            (stream or torch.cuda.current_stream()).synchronize()
         return B, C
 
     # ------------------------------------------------------------------ test / debug

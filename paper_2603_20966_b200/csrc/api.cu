@@ -35,6 +35,10 @@ struct sk_sketch_s {
     std::mutex prof_mu;
     std::vector<sk_timed_launch> prof;
     std::vector<cudaEvent_t> event_pool;  // reused by LaunchScope (no create/destroy per launch)
+    // host streaming: internal copy stream + events (created on first use, per handle)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_join = nullptr;
+    std::mutex host_mu;
 };
 
 static cudaEvent_t pool_get(sk_sketch_s* h) {
@@ -464,6 +468,11 @@ sk_status_t sketch_destroy(sk_sketch_t h) {
     if (h) {
         for (auto& t : h->prof) { cudaEventDestroy(t.start); cudaEventDestroy(t.end); }
         for (auto e : h->event_pool) cudaEventDestroy(e);
+        if (h->copy_stream) {
+            for (int i = 0; i < 2; ++i) { cudaEventDestroy(h->ev_h2d[i]); cudaEventDestroy(h->ev_done[i]); }
+            cudaEventDestroy(h->ev_join);
+            cudaStreamDestroy(h->copy_stream);
+        }
         delete h;
     }
     return SK_SUCCESS;
@@ -652,6 +661,133 @@ sk_status_t sketch_debug_box_muller(const uint32_t* w1, const uint32_t* w2, int6
     cudaError_t e = sk::launch_debug_box_muller(w1, w2, n, transform == SK_OMEGA_FAST, out_even,
                                                 out_odd, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "debug_box_muller launch");
+}
+
+// ------------------------------------------------------------------------------- host streaming
+static int64_t host_block_rows(int64_t n1, int64_t block_rows) {
+    int64_t b = block_rows > 0 ? block_rows : 8192;
+    b = std::min<int64_t>(b, std::max<int64_t>(n1, 1));
+    return round_up(b, 4);
+}
+
+struct HostWs {
+    size_t a_off[2], b_off[2], cacc_off, cpart_off, inner_off, total, a_elems, ld_dev;
+};
+
+static HostWs host_ws_layout(sk_sketch_s* h, int64_t n1, int64_t n2, int64_t block_rows) {
+    HostWs W{};
+    const int64_t br = host_block_rows(n1, block_rows);
+    W.ld_dev = static_cast<size_t>(round_up(n2, 4));
+    W.a_elems = static_cast<size_t>(br) * W.ld_dev;
+    size_t inner = 0;
+    sketch_workspace_size(h, br, &inner);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = round_up(static_cast<int64_t>(off + bytes), 256); return o; };
+    for (int i = 0; i < 2; ++i) W.a_off[i] = take(W.a_elems * sizeof(float));
+    for (int i = 0; i < 2; ++i) W.b_off[i] = take(static_cast<size_t>(br) * h->r * sizeof(float));
+    W.cacc_off = take(static_cast<size_t>(h->r) * h->r * sizeof(float));
+    W.cpart_off = take(static_cast<size_t>(h->r) * h->r * sizeof(float));
+    W.inner_off = take(inner);
+    W.total = off;
+    return W;
+}
+
+static sk_status_t host_stream_impl(sk_sketch_s* h, const float* A, int64_t n1, int64_t n2, int64_t lda,
+                                    float* B, int64_t ldb, float* C, int64_t ldc, int64_t block_rows,
+                                    void* ws, size_t ws_bytes, cudaStream_t s) {
+    const HostWs W = host_ws_layout(h, n1, n2, block_rows);
+    if (ws_bytes < W.total || !ws) return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_host_workspace_size");
+    if (!aligned16(ws)) return fail(SK_ERR_ALIGNMENT, "workspace must be 16-byte aligned");
+    std::lock_guard<std::mutex> g(h->host_mu);
+    if (!h->copy_stream) {
+        if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "copy stream");
+        for (int i = 0; i < 2; ++i) {
+            cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&h->ev_done[i], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+    }
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    const int64_t br = host_block_rows(n1, block_rows);
+    const size_t inner_bytes = W.total - W.inner_off;
+    float* Cacc = reinterpret_cast<float*>(base + W.cacc_off);
+    float* Cpart = reinterpret_cast<float*>(base + W.cpart_off);
+    cudaError_t e;
+    // the copy stream starts after everything already enqueued on `s`
+    if ((e = cudaEventRecord(h->ev_join, s)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaStreamWaitEvent(h->copy_stream, h->ev_join, 0)) != cudaSuccess) return cuda_fail(e, "event");
+    const int64_t nblk = (n1 + br - 1) / br;
+    for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int slot = static_cast<int>(bi & 1);
+        const int64_t r0 = bi * br, rows = std::min(br, n1 - r0);
+        float* Ad = reinterpret_cast<float*>(base + W.a_off[slot]);
+        float* Bd = reinterpret_cast<float*>(base + W.b_off[slot]);
+        // H2D of block bi on the copy stream, once the compute that used this slot is done
+        if (bi >= 2 && (e = cudaStreamWaitEvent(h->copy_stream, h->ev_done[slot], 0)) != cudaSuccess)
+            return cuda_fail(e, "event");
+        e = cudaMemcpy2DAsync(Ad, W.ld_dev * sizeof(float), A + r0 * lda, lda * sizeof(float),
+                              n2 * sizeof(float), rows, cudaMemcpyHostToDevice, h->copy_stream);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D of an A block");
+        if ((e = cudaEventRecord(h->ev_h2d[slot], h->copy_stream)) != cudaSuccess) return cuda_fail(e, "event");
+        // sketch (and core) of block bi on the caller's stream
+        if ((e = cudaStreamWaitEvent(s, h->ev_h2d[slot], 0)) != cudaSuccess) return cuda_fail(e, "event");
+        if (sk_status_t st = apply_impl(h, Ad, rows, n2, static_cast<int64_t>(W.ld_dev), 0, Bd, h->r,
+                                        base + W.inner_off, inner_bytes, s))
+            return st;
+        if (C) {
+            if (sk_status_t st = core_impl(h, Bd, rows, h->r, r0, Cpart, h->r, base + W.inner_off, s)) return st;
+            LaunchScope ls(h, SK_PHASE_CORE_REDUCE, s);
+            if ((e = sk::launch_accumulate(Cacc, Cpart, h->r * h->r, bi == 0, s)) != cudaSuccess)
+                return cuda_fail(e, "accumulate C");
+        }
+        e = cudaMemcpy2DAsync(B + r0 * ldb, ldb * sizeof(float), Bd, h->r * sizeof(float), h->r * sizeof(float),
+                              rows, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H of a B block");
+        if ((e = cudaEventRecord(h->ev_done[slot], s)) != cudaSuccess) return cuda_fail(e, "event");
+    }
+    if (C) {
+        e = cudaMemcpy2DAsync(C, ldc * sizeof(float), Cacc, h->r * sizeof(float), h->r * sizeof(float), h->r,
+                              cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H of C");
+    }
+    // join: `s` also waits for the copy stream's last operation
+    if ((e = cudaEventRecord(h->ev_join, h->copy_stream)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaStreamWaitEvent(s, h->ev_join, 0)) != cudaSuccess) return cuda_fail(e, "event");
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_host_workspace_size(sk_sketch_t h, int64_t n1, int64_t block_rows, size_t* bytes) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (!bytes || n1 < 0) return fail(SK_ERR_INVALID_VALUE, "bad workspace query");
+    *bytes = host_ws_layout(h, std::max<int64_t>(n1, 1), h->n2, block_rows).total;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_apply_host(sk_sketch_t h, const float* A_host, int64_t n1, int64_t n2, int64_t lda,
+                              float* B_host, int64_t ldb, int64_t block_rows, void* ws,
+                              size_t ws_bytes, void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (sk_status_t st = check_mode(h)) return st;
+    if (n2 != h->n2) return fail(SK_ERR_SHAPE_MISMATCH, "n2 != handle n2");
+    if (n1 < 0) return fail(SK_ERR_INVALID_VALUE, "n1 < 0");
+    if (n1 > 0 && (!A_host || !B_host)) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if (lda < n2 || ldb < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "lda < n2 or ldb < r");
+    if (n1 == 0) return SK_SUCCESS;
+    return host_stream_impl(h, A_host, n1, n2, lda, B_host, ldb, nullptr, 0, block_rows, ws, ws_bytes,
+                            static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t nystrom_core_host(sk_sketch_t h, const float* A_host, int64_t n, int64_t lda,
+                              float* B_host, int64_t ldb, float* C_host, int64_t ldc,
+                              int64_t block_rows, void* ws, size_t ws_bytes, void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (sk_status_t st = check_mode(h)) return st;
+    if (n != h->n2) return fail(SK_ERR_SHAPE_MISMATCH, "n != handle n2 (A must be n2 x n2)");
+    if (!A_host || !B_host || !C_host) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if (lda < n || ldb < h->r || ldc < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "lda / ldb / ldc too small");
+    return host_stream_impl(h, A_host, n, n, lda, B_host, ldb, C_host, ldc, block_rows, ws, ws_bytes,
+                            static_cast<cudaStream_t>(stream));
 }
 
 const char* sketch_status_string(sk_status_t st) {

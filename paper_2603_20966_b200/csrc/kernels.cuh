@@ -88,6 +88,7 @@ cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaS
 cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
                                 int nacc, int dist, bool fast, cudaStream_t s);
 size_t core_gemm_tc_smem_bytes(int nacc, int npad);
+cudaError_t launch_accumulate(float* acc, const float* part, int64_t n, bool first, cudaStream_t s);
 cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
                                int64_t ldc, cudaStream_t s);
 

@@ -73,6 +73,20 @@ __global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunk
     }
 }
 
+// acc[a, b] (+)= part[a, b] over an r x r block (host streaming: fixed block order).
+__global__ void accumulate_kernel(float* __restrict__ acc, const float* __restrict__ part, int64_t n,
+                                  int first) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        acc[i] = first ? part[i] : acc[i] + part[i];
+}
+
+cudaError_t launch_accumulate(float* acc, const float* part, int64_t n, bool first, cudaStream_t s) {
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 4));
+    accumulate_kernel<<<blocks, 256, 0, s>>>(acc, part, n, first ? 1 : 0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
                                int64_t ldc, cudaStream_t s) {
     const int64_t rr = static_cast<int64_t>(r) * r;
