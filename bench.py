@@ -233,7 +233,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--mode", default="tf32", choices=["tf32", "tf32x3", "bf16"])
+    ap.add_argument("--mode", default="bf16", choices=["tf32", "tf32x3", "bf16"])
     ap.add_argument("--omega", default="accurate", choices=["accurate", "fast"])
     ap.add_argument("--layout", default="row", help="row | col | AxB (p1 x p2)")
     ap.add_argument("--split-k", type=int, default=0)
@@ -241,6 +241,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-other-modes", action="store_true",
+                    help="skip timing the other precision modes / transforms after the main line")
     args = ap.parse_args()
     W = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -347,7 +349,7 @@ def main():
         ach = kern_flops / avg_s_step / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak}
     roof.update({
-        "kernel": "sketch_gemm_kernel (fused Philox/Box-Muller Omega tiles + tcgen05 tf32)",
+        "kernel": f"sketch_gemm_kernel (fused Philox/Box-Muller Omega tiles + tcgen05 {args.mode})",
         "launches_timed": gemm_launches, "avg_launch_ms": avg_s * 1e3,
         "share_of_step": (gemm_ms / max(t_ms, 1e-9)),
         "hbm_frac": (kern_bytes / avg_s_step / 1e9) / peaks["hbm"],
@@ -381,6 +383,42 @@ def main():
                  "measured_bytes_per_rank": comm_bytes},
     }
 
+    # ------------------------------------------------------------------ the other modes (same A, same step)
+    if not args.no_other_modes:
+        others = {}
+        for mode, omega in (("tf32x3", "accurate"), ("tf32", "accurate"), ("tf32", "fast"), ("bf16", "accurate"),
+                            ("bf16", "fast")):
+            if (mode, omega) == (args.mode, args.omega):
+                continue
+            try:
+                loc2 = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=mode, omega=omega)
+                ds2 = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=loc2)
+
+                def step2():
+                    return ds2.nystrom_core(A) if W["nystrom"] else ds2.apply(A)
+
+                for _ in range(2):
+                    step2()
+                torch.cuda.synchronize()
+                barrier()
+                g0 = torch.cuda.Event(enable_timing=True)
+                g1 = torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                for _ in range(max(3, args.steps // 2)):
+                    step2()
+                g1.record(stream)
+                torch.cuda.synchronize()
+                t2 = torch.tensor([g0.elapsed_time(g1) / max(3, args.steps // 2)], dtype=torch.float64,
+                                  device=dev if world > 1 else "cpu")
+                if world > 1:
+                    tdist.all_reduce(t2, op=tdist.ReduceOp.MAX)
+                t2 = float(t2.item())
+                others[f"{mode}/{omega}"] = {"ms_per_step": t2, "value": a_bytes_total / (t2 * 1e-3) / 1e9}
+                del loc2, ds2
+            except Exception as e:  # pragma: no cover
+                others[f"{mode}/{omega}"] = {"error": repr(e)}
+        result["other_modes"] = others
+
     # ------------------------------------------------------------------ parity at full size (sampled)
     if rank == 0 and not args.no_parity:
         try:
@@ -409,12 +447,15 @@ def main():
             import oracle
             cores = os.cpu_count()
             oracle.set_num_threads(cores)
-            probe_rows = A[:8].cpu().numpy()
-            tp, _ = time_oracle(W, probe_rows)
-            nrows = int(max(8, min(A.shape[0], 8 * 12.0 / max(tp, 1e-3))))
-            nrows = min(nrows, 8192)
-            A_rows = A[:nrows].cpu().numpy()
-            t, _ = time_oracle(W, A_rows)
+            # grow the row sample until the oracle runs >= ~10 s (it materialises Omega once per call,
+            # a fixed cost, so a small probe would under-size the sample)
+            nrows, t = 32, 0.0
+            while True:
+                A_rows = A[:nrows].cpu().numpy()
+                t, _ = time_oracle(W, A_rows)
+                if t >= 10.0 or nrows >= min(A.shape[0], 16384):
+                    break
+                nrows = int(min(min(A.shape[0], 16384), max(2 * nrows, nrows * 12.0 / max(t, 1e-3))))
             result["cpu_baseline"] = {
                 "value": nrows * n2 * 4 / t / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
                 "kind": "oracle",
