@@ -166,33 +166,39 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // Omega ring depth: pairs hand every stage across the pair (relay + multicast commit)
     P.o_stages = xa ? 2 : ((P.cg == 2) ? 3 : 2);
     const int budget = sk::sketch_gemm_max_smem() - 2048;
+    // operand stage: [A_lo (tf32x3)] + Omega (+ Omega_lo); bf16 converts A in place in its A stage
     auto ostage_bytes = [&](int nacc) {
         const int otile = (npad_max / P.cg) * 128 * nsubo;
-        return (xa ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
+        return (x3 ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
     };
+    int a_cap = 6;
+    if (bf && P.cg == 2) { a_cap = 3; P.o_stages = 8; }  // bf16 pairs: 3 x 64 KB A, rest Omega ring
+    if (const char* e = getenv("SK_A_STAGES")) a_cap = std::max(1, std::min(8, atoi(e)));    // tuning
     if (const char* e = getenv("SK_O_STAGES")) P.o_stages = std::max(1, std::min(8, atoi(e)));  // tuning
     for (;;) {
         const int a_stage = P.nacc * 128 * ks * 4;
-        P.a_stages = std::min(6, (budget - P.o_stages * ostage_bytes(P.nacc)) / a_stage);
+        P.a_stages = std::min(a_cap, (budget - 2 * ostage_bytes(P.nacc)) / a_stage);
+        P.o_stages = std::max(2, std::min(P.o_stages, (budget - P.a_stages * a_stage) / ostage_bytes(P.nacc)));
         if (P.a_stages >= 2 || P.nacc == 1) break;
         P.nacc = 1;  // make room for >= 2 A stages
     }
     const int a_stage = P.nacc * 128 * ks * 4;
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, xa, olo, ks, nsubo);
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo);
     P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
     // Clusters of two CTA pairs share each generated Omega slice (1024 rows of A per element).
     // Automatic only in bf16 mode, whose 64-wide K steps amortise the extra cross-pair handshake
     // (measured at c2: bf16 3.07 -> 2.29 ms; tf32 / tf32x3 with 32-wide steps were not faster);
     // sketch_set_cta_group(h, 4) forces it in any mode.
-    const bool want_cl = (h->cl_override == 2) || (h->cl_override == 0 && bf);
-    P.cl = (want_cl && P.cg == 2 && P.nacc == 2 && n1 >= 2048 && npad_max % 32 == 0 &&
-            h->dist == sk::kGaussian) ? 2 : 1;
+    const bool want_cl = (h->cl_override >= 2) || (h->cl_override == 0 && bf);
+    const int cl_req = (h->cl_override == 4) ? 4 : 2;
+    P.cl = (want_cl && P.cg == 2 && P.nacc == 2 && n1 >= 1024 * cl_req && npad_max % (16 * cl_req) == 0 &&
+            h->dist == sk::kGaussian) ? cl_req : 1;
     int workers = sk::num_sms() / P.cg;
-    if (P.cl == 2) {
+    if (P.cl > 1) {
         const int mc = sk::sketch_gemm_max_clusters(P.cg, P.nacc, h->dist, h->mode,
                                                     h->omega_transform == SK_OMEGA_FAST, P.cl, P.smem);
         if (mc <= 0) P.cl = 1;
-        else workers = std::min(mc, sk::num_sms() / 4);
+        else workers = std::min(mc, sk::num_sms() / (2 * P.cl));
     }
     const int rows_per_unit = 128 * P.cg * P.nacc * P.cl;
     P.num_mblk = static_cast<int>((n1 + rows_per_unit - 1) / rows_per_unit);
@@ -539,9 +545,10 @@ sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k) {
 
 sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    if (cg < 0 || cg > 4 || cg == 3) return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1, 2 or 4");
-    h->cg_override = (cg == 4) ? 0 : cg;               // 4: pairs + cluster sharing
-    h->cl_override = (cg == 2) ? 1 : (cg == 4) ? 2 : 0;  // 2: pairs without cluster sharing
+    if (!(cg == 0 || cg == 1 || cg == 2 || cg == 4 || cg == 8))
+        return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1, 2, 4 or 8");
+    h->cg_override = (cg >= 4) ? 0 : cg;                                 // 4 / 8: pairs + sharing
+    h->cl_override = (cg == 2) ? 1 : (cg == 4) ? 2 : (cg == 8) ? 4 : 0;  // 2: pairs, no sharing
     return SK_SUCCESS;
 }
 
@@ -553,7 +560,7 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt) {
 
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    h->ablate = flags & 31u;
+    h->ablate = flags & 63u;
     return SK_SUCCESS;
 }
 

@@ -60,6 +60,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+// Wait with a suspend-time hint (ns): the warp sleeps in the barrier unit until the phase completes
+// or the hint expires, instead of re-issuing try_wait -- for the many producer warps, so that their
+// polling does not take issue slots from the TMA / MMA / relay threads.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 20000) {
+    while (!mbar_try_wait_sleep(bar, parity, ns)) {
+    }
+}
 
 // ----------------------------------------------------------------------------- fences
 // Generic-proxy st.shared -> async-proxy (tcgen05.mma operand) visibility.

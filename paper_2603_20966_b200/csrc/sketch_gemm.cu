@@ -68,12 +68,14 @@ template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
     static_assert(CL == 1 || CG == 2, "Omega sharing between pairs needs CTA pairs");
+    static_assert(CL == 1 || CL == 2 || CL == 4, "1, 2 or 4 CTA pairs per cluster");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     constexpr bool X3 = (MODE == kTF32x3);                 // 3xTF32: A_lo and Omega_lo operands
     constexpr bool BF = (MODE == kBF16);                   // bf16 operands, K = 16 per MMA
     constexpr bool XA = X3 || BF;                          // producers transform A in smem
+    constexpr bool ALO = X3;                               // transformed A lives in the operand stage
     constexpr bool OLO = X3 && (DIST != kRademacher);      // +-1 is exact in tf32: no Omega_lo
     constexpr bool ARELAY = (CG == 2) && XA;               // peer A lands on its own barrier
     constexpr bool T64 = (MODE == kTF32) && (CG == 2);    // tf32 pairs: 64-wide K steps
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int KMMA = T64 ? 8 : 4;                      // MMAs (per accumulator) per stage
     const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
     const uint32_t osub = static_cast<uint32_t>(npad_loc) * 128u;  // bytes of one Omega sub-tile
-    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, XA, OLO, KS, NSUBO);
+    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, ALO, OLO, KS, NSUBO);
     uint8_t* sA = smem + L.a_off;
     uint8_t* sO = smem + L.o_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -103,9 +105,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t crank = crank_cl & 1u;                             // rank in the CTA pair
     const uint32_t lead_rank = crank_cl & ~1u;                        // pair leader's cluster rank
     const uint32_t pairq = crank_cl >> 1;                             // pair index in the cluster
-    const uint32_t partner = crank_cl ^ 2u;                           // CL = 2: same half, other pair
     const uint16_t pair_mask = static_cast<uint16_t>(0x3u << lead_rank);
-    const uint16_t partner_pair_mask = static_cast<uint16_t>(0x3u << (lead_rank ^ 2u));
+    // every other pair of the cluster (their stages receive this CTA's Omega rows)
+    const uint16_t partner_pair_mask = static_cast<uint16_t>(((1u << (2 * CL)) - 1u) & ~(0x3u << lead_rank));
     const bool leader = crank == 0;
     const int group = static_cast<int>(blockIdx.x) / (CG * CL);      // worker = pair (or cluster)
     const int ngroups = static_cast<int>(gridDim.x) / (CG * CL);
@@ -124,10 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < p.o_stages; ++s) {
             // CL = 1: own kRngWarps warps; CL = 2: the copier's expect_tx arrival (after gen_done),
             // plus the partner's bulk-copied half as tx bytes.  Leader: + the peer's relayed arrival.
-            mbar_init(&full_o[s], (CL == 2 ? 1 : kRngWarps) + ((CG == 2 && leader) ? 1 : 0));
+            mbar_init(&full_o[s], (CL > 1 ? 1 : kRngWarps) + ((CG == 2 && leader) ? 1 : 0));
             mbar_init(&empty_o[s], 1);
             mbar_init(&gen_done[s], kRngWarps);
-            mbar_init(&pfree[s], 1);
+            mbar_init(&pfree[s], CL > 1 ? CL - 1 : 1);  // one release per partner pair
         }
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, 4 * CG);
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             if constexpr (BF) {
                                 // bf16 A tile (converted by the producers) in the operand stage
-                                const uint64_t abf = sw128_desc(o_base + L.alo_off + a * kATileBytes + k8 * 32, 16, 1024);
+                                const uint64_t abf = sw128_desc(a_base + a * kATileBytes + k8 * 32, 16, 1024);
                                 if constexpr (CG == 2) mma_bf16_pair(d, abf, bdesc, idesc, acc);
                                 else mma_bf16(d, abf, bdesc, idesc, acc);
                             } else {
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (CG == 2) {
                         mma_commit_pair(&empty_a[sa], pair_mask);
                         mma_commit_pair(&empty_o[so], pair_mask);
-                        if constexpr (CL == 2) mma_commit_pair(&pfree[so], partner_pair_mask);
+                        if constexpr (CL > 1) mma_commit_pair(&pfree[so], partner_pair_mask);
                     } else {
                         mma_commit(&empty_a[sa]);
                         mma_commit(&empty_o[so]);
@@ -258,16 +260,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // with a RELAXED cluster-scope arrive (a release.cluster arrive drains in-flight TMA
         // traffic; the relay writes nothing itself).  CL = 2: the copier (leader: warp 3, peer:
         // warp 1) pushes this CTA's Omega half into the partner pair's CTA.
-        const bool is_copier = (CL == 2) && ((leader && warp == 3) || (!leader && warp == 1));
+        const bool is_copier = (CL > 1) && ((leader && warp == 3) || (!leader && warp == 1));
         const bool is_orelay = (CG == 2) && !leader && warp == 2;
         const bool is_arelay = ARELAY && !leader && warp == 3;
         if ((is_copier || is_orelay || is_arelay) && elect_one()) {
             uint64_t* bars_r = is_orelay ? full_o : full_a;
             const uint32_t nst = static_cast<uint32_t>(is_arelay ? p.a_stages : p.o_stages);
-            const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / 2);
-            const uint32_t half_bytes = gen_rows * 128u;
+            const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / CL);
+            const uint32_t half_bytes = gen_rows * 128u;  // this CTA's share of one sub-tile
             const uint32_t half_off = pairq * half_bytes;
-            const uint32_t tx = half_bytes * (OLO ? 2u : 1u) * NSUBO;
+            const uint32_t tx = half_bytes * (OLO ? 2u : 1u) * NSUBO * (CL - 1);
             uint32_t st = 0, ph = 0;
             for (int u = group; u < total_units; u += ngroups) {
                 const int s = u - (u / p.split) * p.split;
@@ -277,15 +279,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&gen_done[st], ph);
                         mbar_arrive_expect_tx(&full_o[st], tx);  // local half done; partner half incoming
                         mbar_wait(&pfree[st], ph ^ 1);
-                        const uint32_t bar = mapa_shared(smem_u32(&full_o[st]), partner);
 #pragma unroll
-                        for (int sb = 0; sb < NSUBO; ++sb) {
-                            const uint32_t src = smem_u32(sO + st * L.o_stage + L.ohi_off) + sb * osub + half_off;
-                            bulk_copy_to_cta(mapa_shared(src, partner), src, half_bytes, bar);
-                        }
-                        if constexpr (OLO) {
-                            const uint32_t src_lo = smem_u32(sO + st * L.o_stage + L.olo_off) + half_off;
-                            bulk_copy_to_cta(mapa_shared(src_lo, partner), src_lo, half_bytes, bar);
+                        for (int pp = 1; pp < CL; ++pp) {
+                            // partner CTA: same half of the pair, pair (pairq + pp) mod CL
+                            const uint32_t partner = ((((pairq + pp) % CL)) << 1) | crank;
+                            const uint32_t bar = mapa_shared(smem_u32(&full_o[st]), partner);
+#pragma unroll
+                            for (int sb = 0; sb < NSUBO; ++sb) {
+                                const uint32_t src = smem_u32(sO + st * L.o_stage + L.ohi_off) + sb * osub + half_off;
+                                bulk_copy_to_cta(mapa_shared(src, partner), src, half_bytes, bar);
+                            }
+                            if constexpr (OLO) {
+                                const uint32_t src_lo = smem_u32(sO + st * L.o_stage + L.olo_off) + half_off;
+                                bulk_copy_to_cta(mapa_shared(src_lo, partner), src_lo, half_bytes, bar);
+                            }
                         }
                     } else {
                         mbar_wait(&bars_r[st], ph);
@@ -299,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= kCtlWarps) {
         // ------------------------------------------------------------------ Omega producers + epilogue
         const int t = static_cast<int>(threadIdx.x) - kCtlWarps * 32;
-        const int gen_rows = (CL == 2) ? npad_loc / 2 : npad_loc;              // rows this CTA generates
-        const int gen_row0 = (CL == 2) ? static_cast<int>(pairq) * gen_rows : 0; // first generated row
+        const int gen_rows = npad_loc / CL;                                      // rows this CTA generates
+        const int gen_row0 = static_cast<int>(pairq) * gen_rows;                 // first generated row
         const int n_start = t % gen_rows, j_start = t / gen_rows;
         const int tq = kRngThreads / gen_rows, tr = kRngThreads % gen_rows;
         const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
@@ -310,7 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int mb = u / p.split, s = u - (u / p.split) * p.split;
             const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
             for (int kit = kb; kit < ke; ++kit) {
-                mbar_wait(&empty_o[so], po ^ 1);
+                if (p.ablate & 32u) mbar_wait(&empty_o[so], po ^ 1);
+                else mbar_wait_sleep(&empty_o[so], po ^ 1);
                 uint8_t* ostage = sO + so * L.o_stage;
                 uint8_t* otile = ostage + L.ohi_off + gen_row0 * 128;  // this CTA's generated rows
                 if (p.ablate & 1u) {
@@ -335,25 +343,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                                p.roff, gen_rows, c0_loc, p.key0, p.key1,
                                                                n_start, j_start, tq, tr, lo_off);
                 if constexpr (BF) {
-                    // A (two fp32 SW128 boxes of 32 K per accumulator) -> one bf16 SW128 tile of 64 K:
-                    // item (acc a, row m, chunk j8 = 8 K-values); a warp covers 32 consecutive rows
+                    // A (two fp32 SW128 boxes of 32 K per accumulator) -> one bf16 SW128 tile of 64 K,
+                    // IN PLACE at the start of the A stage (acc a's tile at a * 16 KB): every producer
+                    // first reads its items into registers, a named barrier over the producer warps,
+                    // then the packed bf16 chunks are written.  Item = (acc a, row m, chunk j8 of 8
+                    // K-values); a warp covers 32 consecutive rows (conflict-free under the swizzle).
+                    constexpr int kItems = NACC * 1024 / kRngThreads;
                     mbar_wait(&full_a[sa], pa);
-                    const uint32_t src0 = smem_u32(sA + sa * L.a_stage);
-                    const uint32_t dst0 = smem_u32(ostage + L.alo_off);
-                    for (int i = t; i < NACC * 1024; i += kRngThreads) {
+                    const uint32_t st0 = smem_u32(sA + sa * L.a_stage);
+                    float4 va[kItems][2];
+#pragma unroll
+                    for (int it = 0; it < kItems; ++it) {
+                        const int i = t + it * kRngThreads;
                         const int a = i >> 10, rem = i & 1023, m = rem & 127, j8 = rem >> 7;
                         const uint32_t sw = static_cast<uint32_t>(m & 7);
                         const uint32_t c0 = 2u * static_cast<uint32_t>(j8 & 3);
-                        const uint32_t row = src0 + static_cast<uint32_t>((a * 2 + (j8 >> 2)) * kATileBytes + m * 128);
-                        float4 v0, v1;
+                        const uint32_t row = st0 + static_cast<uint32_t>((a * 2 + (j8 >> 2)) * kATileBytes + m * 128);
                         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(v0.x), "=f"(v0.y), "=f"(v0.z), "=f"(v0.w) : "r"(row + ((c0 ^ sw) << 4)));
+                                     : "=f"(va[it][0].x), "=f"(va[it][0].y), "=f"(va[it][0].z), "=f"(va[it][0].w)
+                                     : "r"(row + ((c0 ^ sw) << 4)));
                         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(v1.x), "=f"(v1.y), "=f"(v1.z), "=f"(v1.w) : "r"(row + (((c0 + 1) ^ sw) << 4)));
-                        st_shared_v4_u32(dst0 + static_cast<uint32_t>(a * kATileBytes + m * 128) +
+                                     : "=f"(va[it][1].x), "=f"(va[it][1].y), "=f"(va[it][1].z), "=f"(va[it][1].w)
+                                     : "r"(row + (((c0 + 1) ^ sw) << 4)));
+                    }
+                    asm volatile("bar.sync 1, %0;" ::"n"(kRngThreads) : "memory");  // all reads done
+#pragma unroll
+                    for (int it = 0; it < kItems; ++it) {
+                        const int i = t + it * kRngThreads;
+                        const int a = i >> 10, rem = i & 1023, m = rem & 127, j8 = rem >> 7;
+                        const uint32_t sw = static_cast<uint32_t>(m & 7);
+                        st_shared_v4_u32(st0 + static_cast<uint32_t>(a * kATileBytes + m * 128) +
                                              ((static_cast<uint32_t>(j8) ^ sw) << 4),
-                                         pack_bf16x2(v0.x, v0.y), pack_bf16x2(v0.z, v0.w),
-                                         pack_bf16x2(v1.x, v1.y), pack_bf16x2(v1.z, v1.w));
+                                         pack_bf16x2(va[it][0].x, va[it][0].y), pack_bf16x2(va[it][0].z, va[it][0].w),
+                                         pack_bf16x2(va[it][1].x, va[it][1].y), pack_bf16x2(va[it][1].z, va[it][1].w));
                     }
                     if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                 }
@@ -375,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(CL == 2 ? &gen_done[so] : &full_o[so]);
+                if (lane == 0) mbar_arrive(CL > 1 ? &gen_done[so] : &full_o[so]);
                 if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
             }
             if (t < 128) {
@@ -448,8 +470,9 @@ int sketch_gemm_max_smem() { return 227 * 1024; }
 // Clusters of `cluster` CTAs of this kernel that can be co-resident (GPC packing strands SMs for
 // clusters of 4).  Returns 0 if the query fails.
 int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem) {
-    static int cache[4][2] = {{-1, -1}, {-1, -1}, {-1, -1}, {-1, -1}};  // [mode][fast], per process
-    if (mode >= 0 && mode < 4 && cache[mode][fast ? 1 : 0] >= 0) return cache[mode][fast ? 1 : 0];
+    static int cache[3][4][2] = {};  // [cl/2][mode][fast] + 1, per process
+    const int ci = cl == 4 ? 2 : 1;
+    if (mode >= 0 && mode < 4 && cache[ci][mode][fast ? 1 : 0] > 0) return cache[ci][mode][fast ? 1 : 0] - 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cg * cl * 64);
     cfg.blockDim = dim3(kThreads);
@@ -463,18 +486,22 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
     cfg.numAttrs = 1;
     int n = 0;
     const void* fn = nullptr;
-#define SK_FN(M, F) fn = reinterpret_cast<const void*>(sketch_gemm_kernel<2, 2, kGaussian, M, F, 2>)
-    if (cg == 2 && cl == 2 && nacc == 2 && dist == kGaussian) {
-        if (mode == kTF32) { if (fast) SK_FN(kTF32, true); else SK_FN(kTF32, false); }
-        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true); else SK_FN(kBF16, false); }
-        else SK_FN(kTF32x3, false);
+#define SK_FN(M, F, C) fn = reinterpret_cast<const void*>(sketch_gemm_kernel<2, 2, kGaussian, M, F, C>)
+    if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 2) {
+        if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 2); else SK_FN(kTF32, false, 2); }
+        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 2); else SK_FN(kBF16, false, 2); }
+        else SK_FN(kTF32x3, false, 2);
+    } else if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 4) {
+        if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 4); else SK_FN(kTF32, false, 4); }
+        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 4); else SK_FN(kBF16, false, 4); }
+        else SK_FN(kTF32x3, false, 4);
     }
 #undef SK_FN
     if (!fn) return 0;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
         return 0;
     if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) return 0;
-    if (mode >= 0 && mode < 4) cache[mode][fast ? 1 : 0] = n;
+    if (mode >= 0 && mode < 4) cache[ci][mode][fast ? 1 : 0] = n + 1;
     return n;
 }
 
@@ -531,6 +558,7 @@ static cudaError_t dispatch_dist(const CUtensorMap& tmA, const SketchGemmParams&
 cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg, int nacc,
                                int dist, int mode, bool fast, int grid, size_t smem,
                                cudaStream_t s, int cl) {
+    if (cl == 4 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 4>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cl == 2 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cl == 2 && cg == 2 && nacc == 1) return dispatch_dist<2, 1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cg == 1 && nacc == 1) return dispatch_dist<1, 1>(tmA, p, dist, mode, fast, grid, smem, s);

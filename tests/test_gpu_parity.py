@@ -304,10 +304,11 @@ def test_cluster_sharing_bit_identical(mode, omega):
     sk = _sk()
     A = _dev(synth.uniform(21, 4100, 3000))
     outs = []
-    for cg in (2, 4):
+    for cg in (2, 4, 8):
         s = sk.Sketch(SEED, "gaussian", 3000, 256, mode=mode, omega=omega, cta_group=cg, split_k=3)
         outs.append(s.apply(A))
     assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[2])
 
 
 @pytest.mark.parametrize("block_rows", [0, 100, 333])
