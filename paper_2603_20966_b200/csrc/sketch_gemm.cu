@@ -126,7 +126,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < p.o_stages; ++s) {
             // CL = 1: own kRngWarps warps; CL = 2: the copier's expect_tx arrival (after gen_done),
             // plus the partner's bulk-copied half as tx bytes.  Leader: + the peer's relayed arrival.
-            mbar_init(&full_o[s], (CL > 1 ? 1 : kRngWarps) + ((CG == 2 && leader) ? 1 : 0));
+            // CL = 1 pairs: the peer's producer warps arrive directly (relaxed, remote) on the leader
+            mbar_init(&full_o[s], (CL > 1) ? (1 + (leader ? 1 : 0))
+                                           : (CG == 2 ? (leader ? 2 * kRngWarps : kRngWarps) : kRngWarps));
             mbar_init(&empty_o[s], 1);
             mbar_init(&gen_done[s], kRngWarps);
             mbar_init(&pfree[s], CL > 1 ? CL - 1 : 1);  // one release per partner pair
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // traffic; the relay writes nothing itself).  CL = 2: the copier (leader: warp 3, peer:
         // warp 1) pushes this CTA's Omega half into the partner pair's CTA.
         const bool is_copier = (CL > 1) && ((leader && warp == 3) || (!leader && warp == 1));
-        const bool is_orelay = (CG == 2) && !leader && warp == 2;
+        const bool is_orelay = (CG == 2) && (CL > 1) && !leader && warp == 2;
         const bool is_arelay = ARELAY && !leader && warp == 3;
         if ((is_copier || is_orelay || is_arelay) && elect_one()) {
             uint64_t* bars_r = is_orelay ? full_o : full_a;
@@ -397,7 +399,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(CL > 1 ? &gen_done[so] : &full_o[so]);
+                if (lane == 0) {
+                    if constexpr (CL > 1) mbar_arrive(&gen_done[so]);
+                    else if (CG == 2 && !leader) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&full_o[so]), lead_rank));
+                    else mbar_arrive(&full_o[so]);
+                }
                 if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
             }
             if (t < 128) {
