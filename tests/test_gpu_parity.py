@@ -338,3 +338,30 @@ def test_host_streaming_nystrom_integer_exact(block_rows):
     Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, 64)
     assert np.array_equal(B.numpy().astype(np.float64), Bref)
     assert np.array_equal(C.numpy().astype(np.float64), Cref)
+
+
+def test_nystrom_reconstruction_exact_rank():
+    """f3: rank-20 PSD A, r = 40: B C^+ B^T recovers A (PAPER.md:121, pinv tol 1e-12 PAPER.md:1020);
+    the blocked error formula agrees with the explicit reconstruction."""
+    sk = _sk()
+    from paper_2603_20966_b200 import quality
+    A, _ = synth.lowrank_psd(3, 1200, 20)
+    Ad = _dev(A)
+    s = sk.Sketch(SEED, "gaussian", 1200, 40, mode="tf32x3")
+    B, C = s.nystrom_core(Ad)
+    err = quality.reconstruction_error(Ad, B, C, block_rows=500)
+    W = quality.pinv_sym(C)
+    explicit = torch.linalg.norm(Ad.double() - B.double() @ W @ B.double().T) / torch.linalg.norm(Ad.double())
+    assert err < 1e-4 and abs(err - float(explicit)) < 1e-6
+
+
+def test_nystrom_error_decreases_with_rank_gpu():
+    sk = _sk()
+    from paper_2603_20966_b200 import quality
+    Ad = _dev(synth.rbf_kernel(4, 1500, 8))
+    errs = []
+    for r in (16, 64, 192):
+        s = sk.Sketch(SEED, "gaussian", 1500, r, mode="tf32x3")
+        B, C = s.nystrom_core(Ad)
+        errs.append(quality.reconstruction_error(Ad, B, C))
+    assert errs[0] > errs[1] > errs[2]
