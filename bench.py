@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--omega", default="accurate", choices=["accurate", "fast"])
     ap.add_argument("--layout", default="row", help="row | col | AxB (p1 x p2)")
     ap.add_argument("--split-k", type=int, default=0)
+    ap.add_argument("--variant", default="noredist", choices=["noredist", "redist"],
+                    help="Alg. 2 variant for N > 1 row-block Nystrom (PAPER.md:698)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -281,6 +283,8 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
+        if W["nystrom"] and args.variant == "redist" and world > 1:
+            return ds.nystrom_core_redist(A)
         if W["nystrom"]:
             return ds.nystrom_core(A)
         Bp, rows = ds.apply(A)
@@ -379,7 +383,9 @@ def main():
         "gpu_launches": launches,
         "host_submit_ms_per_step": host_ms,
         "clocks": clocks,
-        "comm": {"predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"]),
+        "comm": {"variant": args.variant if (W["nystrom"] and world > 1) else None,
+                 "predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"],
+                                                                     args.variant if world > 1 else "noredist"),
                  "measured_bytes_per_rank": comm_bytes},
     }
 

@@ -132,6 +132,12 @@ sk_status_t sketch_apply_block(sk_sketch_t h, const float* A_blk, int64_t m, int
 sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb,
                              int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
                              void* stream);
+/* Column-block form for the Redist variant of Alg. 2 (Psi = (1,1,P)): B_blk holds
+ * nb (1 <= nb <= r) columns of B for rows i0 .. i0+m-1, and C_part[r x nb] = Omega[i0:i0+m, 0:r]^T B_blk
+ * is the matching column block of C.  Workspace as for core_apply_block. */
+sk_status_t core_apply_block_cols(sk_sketch_t h, const float* B_blk, int64_t m, int64_t nb,
+                                  int64_t ldb, int64_t i0, float* C_part, int64_t ldc, void* ws,
+                                  size_t ws_bytes, void* stream);
 
 /* Host-buffer / out-of-core forms: A, B and C are HOST pointers (page-locked memory --
  * cudaHostAlloc / cudaHostRegister -- gives full PCIe bandwidth; pageable memory works but the

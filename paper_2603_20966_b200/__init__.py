@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
-    "sketch_apply_block", "core_apply_block", "sketch_generate", "sketch_generate_bits",
+    "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
@@ -77,6 +77,7 @@ def load_library(build_if_missing: bool = True):
         lib.nystrom_core.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, vp, sz, vp]
         lib.sketch_apply_block.argtypes = [vp, vp, i64, i64, i64, i64, vp, i64, vp, sz, vp]
         lib.core_apply_block.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, sz, vp]
+        lib.core_apply_block_cols.argtypes = [vp, vp, i64, i64, i64, i64, vp, i64, vp, sz, vp]
         lib.sketch_host_workspace_size.argtypes = [vp, i64, i64, ctypes.POINTER(sz)]
         lib.sketch_apply_host.argtypes = [vp, vp, i64, i64, i64, vp, i64, i64, vp, sz, vp]
         lib.nystrom_core_host.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, i64, vp, sz, vp]
@@ -248,6 +249,19 @@ class Sketch:
         _check(self._lib.core_apply_block(self._h, B_blk.data_ptr(), m, B_blk.stride(0), int(i0),
                                           out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
                                           _stream_ptr(stream)))
+        return out
+
+    def core_block_cols(self, B_blk, i0: int, out=None, stream=None):
+        """C[:, cols] = Omega[i0:i0+m]^T B_blk for a column block of B (Redist variant)."""
+        torch = _torch()
+        _require_cuda(B_blk, out)
+        m, nb = B_blk.shape
+        if out is None:
+            out = torch.empty((self.r, nb), dtype=torch.float32, device=B_blk.device)
+        ws = self.workspace(m, B_blk.device)
+        _check(self._lib.core_apply_block_cols(self._h, B_blk.data_ptr(), m, nb, B_blk.stride(0), int(i0),
+                                               out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
+                                               _stream_ptr(stream)))
         return out
 
     def nystrom_core(self, A, B=None, C=None, stream=None):

@@ -359,29 +359,31 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
 
 // C[r x r] (ldc) = Omega[i0 : i0+m, :r]^T * B[m x r]
 sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, int64_t i0,
-                      float* C, int64_t ldc, void* ws, cudaStream_t stream) {
+                      float* C, int64_t ldc, void* ws, cudaStream_t stream, int64_t nb = -1) {
+    if (nb < 0) nb = h->r;
     CorePlan CP = plan_core(h, m, i0);
     if (CP.tc && (!aligned16(B) || (ldb & 3))) CP = plan_core_simt(h, m);  // TMA needs 16-B rows
     if (CP.tc && m > 0) {
         CUtensorMap map;
-        if (sk_status_t st = make_map_2d(&map, B, m, h->r, ldb, 32, 32, false)) return st;
+        if (sk_status_t st = make_map_2d(&map, B, m, nb, ldb, 32, 32, false)) return st;
         sk::CoreTcParams q{};
         q.part = static_cast<float*>(ws);
-        q.ldp = h->r;
+        q.ldp = nb;
         q.i0 = i0;
         q.base = CP.base;
         q.step = CP.step;
         q.m = static_cast<int32_t>(m);
         q.r = static_cast<int32_t>(h->r);
-        q.npad = CP.npad;
+        q.nb = static_cast<int32_t>(nb);
+        q.npad = static_cast<int32_t>(round_up(nb, 16));
         q.nchunks = CP.chunks;
         q.key0 = static_cast<uint32_t>(h->seed);
         q.key1 = static_cast<uint32_t>(h->seed >> 32);
         // partials [nchunks * r, r] stored by TMA in 32x32 tiles when r is a multiple of 32
         CUtensorMap omap;
-        q.tma_store = (h->r % 32 == 0 && aligned16(ws)) ? 1 : 0;
+        q.tma_store = (h->r % 32 == 0 && nb % 4 == 0 && aligned16(ws)) ? 1 : 0;
         if (q.tma_store) {
-            if (sk_status_t st = make_map_2d(&omap, q.part, static_cast<int64_t>(q.nchunks) * h->r, h->r, h->r, 32, 32))
+            if (sk_status_t st = make_map_2d(&omap, q.part, static_cast<int64_t>(q.nchunks) * h->r, nb, nb, 32, 32))
                 return st;
         } else {
             omap = map;  // unused
@@ -394,7 +396,7 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         if (e != cudaSuccess) return cuda_fail(e, "core_gemm_tc launch");
         {
             LaunchScope ls(h, SK_PHASE_CORE_REDUCE, stream);
-            e = sk::launch_core_reduce(q.part, q.nchunks, q.r, C, ldc, stream);
+            e = sk::launch_core_reduce(q.part, q.nchunks, q.r, q.nb, C, ldc, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "core_reduce launch");
         return SK_SUCCESS;
@@ -403,16 +405,17 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
     p.B = B;
     p.ldb = ldb;
     p.part = static_cast<float*>(ws);
-    p.ldp = h->r;
+    p.ldp = nb;
     p.i0 = i0;
     p.m = static_cast<int32_t>(m);
     p.r = static_cast<int32_t>(h->r);
+    p.nb = static_cast<int32_t>(nb);
     p.chunk_rows = CP.chunk_rows;
     p.chunks = CP.chunks;
     p.key0 = static_cast<uint32_t>(h->seed);
     p.key1 = static_cast<uint32_t>(h->seed >> 32);
     if (m == 0) {
-        cudaError_t e = cudaMemset2DAsync(C, ldc * sizeof(float), 0, h->r * sizeof(float), h->r, stream);
+        cudaError_t e = cudaMemset2DAsync(C, ldc * sizeof(float), 0, nb * sizeof(float), h->r, stream);
         return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "memset C");
     }
     cudaError_t e;
@@ -423,7 +426,7 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
     if (e != cudaSuccess) return cuda_fail(e, "core_gemm launch");
     {
         LaunchScope ls(h, SK_PHASE_CORE_REDUCE, stream);
-        e = sk::launch_core_reduce(p.part, p.chunks, p.r, C, ldc, stream);
+        e = sk::launch_core_reduce(p.part, p.chunks, p.r, p.nb, C, ldc, stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "core_reduce launch");
     return SK_SUCCESS;
@@ -621,6 +624,22 @@ sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64
     if (ws_bytes < need || !ws)
         return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_workspace_size");
     return core_impl(h, B_blk, m, ldb, i0, C_part, ldc, ws, static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t core_apply_block_cols(sk_sketch_t h, const float* B_blk, int64_t m, int64_t nb, int64_t ldb,
+                                  int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (sk_status_t st = check_mode(h)) return st;
+    if (m < 0 || i0 < 0 || i0 + m > h->n2)
+        return fail(SK_ERR_SHAPE_MISMATCH, "Omega rows [i0, i0+m) exceed the handle's n2");
+    if (nb < 1 || nb > h->r) return fail(SK_ERR_INVALID_VALUE, "nb must be in [1, r]");
+    if ((m > 0 && !B_blk) || !C_part) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if (ldb < nb || ldc < nb) return fail(SK_ERR_SHAPE_MISMATCH, "ldb / ldc < nb");
+    const size_t need = core_ws_bytes(h, std::max<int64_t>(m, 1));
+    if (ws_bytes < need || !ws)
+        return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_workspace_size");
+    return core_impl(h, B_blk, m, ldb, i0, C_part, ldc, ws, static_cast<cudaStream_t>(stream), nb);
 }
 
 sk_status_t nystrom_core(sk_sketch_t h, const float* A, int64_t n, int64_t lda, float* B,

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256)
         // B rows rb..rb+31, cols b0..b0+63
         for (int e = threadIdx.x; e < kCK * kCT; e += 256) {
             const int i = e / kCT, c = e % kCT;
-            sB[i][c] = (i < nr && b0 + c < p.r) ? p.B[static_cast<int64_t>(rb + i) * p.ldb + b0 + c] : 0.f;
+            sB[i][c] = (i < nr && b0 + c < p.nb) ? p.B[static_cast<int64_t>(rb + i) * p.ldb + b0 + c] : 0.f;
         }
         // Omega rows (global) g0..g0+nr-1, cols a0..a0+63
         const int64_t g0 = p.i0 + rb;
@@ -93,14 +93,13 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int b = b0 + tx * 4 + v;
-            if (b < p.r) out[static_cast<int64_t>(a) * p.ldp + b] = acc[u][v];
+            if (b < p.nb) out[static_cast<int64_t>(a) * p.ldp + b] = acc[u][v];
         }
     }
 }
 
 cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaStream_t s) {
-    const int t = (p.r + kCT - 1) / kCT;
-    dim3 grid(t, t, p.chunks);
+    dim3 grid((p.r + kCT - 1) / kCT, (p.nb + kCT - 1) / kCT, p.chunks);
     if (dist == kRademacher) core_gemm_simt_kernel<kRademacher, false><<<grid, 256, 0, s>>>(p);
     else if (dist == kUniform) core_gemm_simt_kernel<kUniform, false><<<grid, 256, 0, s>>>(p);
     else if (fast) core_gemm_simt_kernel<kGaussian, true><<<grid, 256, 0, s>>>(p);
@@ -300,7 +299,7 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
                     } else if (row < p.r) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
-                            if (cc + i < p.r) orow[cc + i] = __uint_as_float(v[i]);
+                            if (cc + i < p.nb) orow[cc + i] = __uint_as_float(v[i]);
                     }
                 }
             }

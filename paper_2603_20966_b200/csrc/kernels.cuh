@@ -40,7 +40,8 @@ struct CoreGemmParams {
     int64_t ldp;          // row stride of a partial (elements)
     int64_t i0;           // global Omega row of B row 0
     int32_t m;            // rows of B
-    int32_t r;
+    int32_t r;            // Omega columns = rows of C
+    int32_t nb;           // columns of B = columns of C (r for the Nystrom core, r/P for Redist)
     int32_t chunk_rows;   // rows of B per CTA chunk
     int32_t chunks;
     uint32_t key0, key1;
@@ -55,8 +56,9 @@ struct CoreTcParams {
     int64_t base;         // i0 rounded down to 128
     int64_t step;         // rows per chunk (multiple of 128)
     int32_t m;            // rows of B
-    int32_t r;
-    int32_t npad;         // MMA N (multiple of 16, <= 256)
+    int32_t r;            // Omega columns = rows of C
+    int32_t nb;           // columns of B = columns of C
+    int32_t npad;         // MMA N = nb padded (multiple of 16, <= 256)
     int32_t nchunks;
     int32_t tma_store;    // 1: epilogue stores 32x32 tiles with TMA through tmOut (r % 32 == 0)
     uint32_t key0, key1;
@@ -89,7 +91,7 @@ cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CUtensorMap& tmOut
                                 int nacc, int dist, bool fast, cudaStream_t s);
 size_t core_gemm_tc_smem_bytes(int nacc, int npad);
 cudaError_t launch_accumulate(float* acc, const float* part, int64_t n, bool first, cudaStream_t s);
-cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
+cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, int32_t nb, float* C,
                                int64_t ldc, cudaStream_t s);
 
 cudaError_t launch_generate(uint64_t seed, int dist, int64_t row0, int64_t nrows, int64_t col0,

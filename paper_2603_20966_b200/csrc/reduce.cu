@@ -61,15 +61,15 @@ cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t
     return cudaGetLastError();
 }
 
-// C[a, b] = sum_{c < chunks} part[c][a][b], r x r, fixed order.
-__global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r,
+// C[a, b] = sum_{c < chunks} part[c][a][b], r x nb, fixed order.
+__global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r, int32_t nb,
                                    float* __restrict__ C, int64_t ldc) {
-    const int64_t rr = static_cast<int64_t>(r) * r;
+    const int64_t rr = static_cast<int64_t>(r) * nb;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < rr;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float acc = 0.f;
         for (int c = 0; c < chunks; ++c) acc += __ldg(part + c * rr + idx);
-        C[(idx / r) * ldc + idx % r] = acc;
+        C[(idx / nb) * ldc + idx % nb] = acc;
     }
 }
 
@@ -87,11 +87,11 @@ cudaError_t launch_accumulate(float* acc, const float* part, int64_t n, bool fir
     return cudaGetLastError();
 }
 
-cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, float* C,
+cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, int32_t nb, float* C,
                                int64_t ldc, cudaStream_t s) {
-    const int64_t rr = static_cast<int64_t>(r) * r;
+    const int64_t rr = static_cast<int64_t>(r) * nb;
     const int blocks = static_cast<int>(std::min<int64_t>((rr + 255) / 256, 148 * 8));
-    core_reduce_kernel<<<blocks, 256, 0, s>>>(part, chunks, r, C, ldc);
+    core_reduce_kernel<<<blocks, 256, 0, s>>>(part, chunks, r, nb, C, ldc);
     return cudaGetLastError();
 }
 

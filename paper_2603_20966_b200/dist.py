@@ -15,6 +15,14 @@ Implements Alg. 1 (RandMatMul) and the No-Redist variant of Al
     then AllReduce of the r x r partials (the GPU variant replaces Reduce-Scatter
     of C by AllReduce; reading R11: full C on every rank).
 
+Redist variant (Case 1 of the first grid-selection approach, p1 = q3 = P,
+PAPER.md:665-687, 698): B is computed row-block (zero communication), redistributed by an All-to-All
+so that rank k owns column block k of B over all n rows (bandwidth ~ n r / P words, PAPER.md:675;
+the pack / unpack of the paper's column-major exchange, is a strided copy here), and
+rank k computes the column block C[:, cols_k] = Omega^T B[:, cols_k] with Omega regenerated for all n
+rows.  The paper leaves C distributed; `nystrom_core_redist` all-gathers the column blocks so both
+variants return the same replicated C.
+
 Bandwidth accounting: predicted words per rank = (1 - 1/p2) n1 r / p1 for B (Alg. 1 cost,
 PAPER.md:427 with p3 = 1) plus the AllReduce payload r^2 for C; measured = bytes handed to
 the collectives.  Row splits are balanced; column splits are multiples of 128 (so each block's
@@ -61,10 +69,16 @@ class Layout:
         return Layout(a, b)
 
 
-def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool) -> int:
-    """Alg. 1 reduce-scatter volume (1 - 1/p2) n1 r / p1 words (+ r^2 AllReduce payload), fp32."""
+def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool, variant: str = "noredist") -> int:
+    """Alg. 1 reduce-scatter volume (1 - 1/p2) n1 r / p1 words (+ r^2 AllReduce payload), fp32.
+    Redist (row-block only): All-to-All of B, (1 - 1/P) n r / P words sent per rank,
+    plus the all-gather that replicates C, (P - 1) r ceil(r / P) words."""
+    P = layout.P
+    if variant == "redist" and nystrom and P > 1:
+        return int(4 * ((n1 * r) // P - (n1 // P) * (r // P) + (P - 1) * r * (-(-r // P)))) if (n1 % P == 0 and r % P == 0) \
+            else -1
     words = (1.0 - 1.0 / layout.p2) * n1 * r / layout.p1
-    if nystrom and layout.P > 1:
+    if nystrom and P > 1:
         words += r * r
     return int(round(4 * words))
 
@@ -137,6 +151,39 @@ class DistSketch:
         self.comm_bytes += Bbar.numel() * 4 * (p2 - 1) // p2
         a, b = self.b_piece_rows()
         return piece[: b - a], (a, b)
+
+    # ------------------------------------------------------------------ Alg. 2 (Redist)
+    def nystrom_core_redist(self, A_blk):
+        """Redist variant: returns (B_piece, rows, C) like nystrom_core (row-block layout only)."""
+        import torch
+        if self.layout.p2 != 1:
+            raise ValueError("the Redist variant runs on the row-block grid Pi = (P, 1, 1)")
+        Bp, (a, b) = self.apply(A_blk)
+        P, r = self.world, self.r
+        if P == 1:
+            return Bp, (a, b), self.local.core_block(Bp, a)
+        cb = balanced_split(r, P)
+        k = self.rank
+        nbk = cb[k + 1] - cb[k]
+        rows = [self.row_bnd[j + 1] - self.row_bnd[j] for j in range(P)]
+        send = torch.cat([Bp[:, cb[j]:cb[j + 1]].reshape(-1) for j in range(P)])  # pack by column block
+        in_splits = [(b - a) * (cb[j + 1] - cb[j]) for j in range(P)]
+        out_splits = [rows[j] * nbk for j in range(P)]
+        recv = torch.empty(sum(out_splits), dtype=torch.float32, device=Bp.device)
+        self.tdist.all_to_all_single(recv, send, out_splits, in_splits, group=self.group)
+        self.comm_bytes += 4 * (sum(in_splits) - in_splits[k])
+        Bcol = recv.view(self.n1, nbk)  # rows arrive in rank order = global row order
+        Ccol = self.local.core_block_cols(Bcol, 0)  # r x nbk, Omega regenerated for all n rows
+        # replicate C: all-gather the column blocks (padded to the largest block)
+        width = max(cb[j + 1] - cb[j] for j in range(P))
+        pad = torch.zeros((r, width), dtype=torch.float32, device=Bp.device)
+        pad[:, :nbk] = Ccol
+        gathered = torch.empty(P * r * width, dtype=torch.float32, device=Bp.device)
+        self.tdist.all_gather_into_tensor(gathered, pad.reshape(-1), group=self.group)
+        gathered = gathered.view(P, r, width)
+        self.comm_bytes += 4 * r * width * (P - 1)
+        C = torch.cat([gathered[j, :, : cb[j + 1] - cb[j]] for j in range(P)], dim=1)
+        return Bp, (a, b), C
 
     # ------------------------------------------------------------------ Alg. 2 (No-Redist)
     def nystrom_core(self, A_blk):

@@ -34,6 +34,13 @@ class OracleLocal:
         out.copy_(B)
         return out
 
+    def core_block_cols(self, B_blk, i0):
+        # C[:, cols] = Omega[i0:i0+m, :r]^T B_blk (nb columns): the oracle core on a zero-padded B
+        m, nb = B_blk.shape
+        Bpad = np.zeros((m, self.r), dtype=np.float64)
+        Bpad[:, :nb] = B_blk.numpy()
+        return torch.from_numpy(oracle.core(self.seed, self.dist, Bpad, i0=i0)[:, :nb].astype(np.float32))
+
     def core_block(self, B_blk, i0):
         return torch.from_numpy(oracle.core(self.seed, self.dist, B_blk.numpy().astype(np.float64), i0=i0).astype(np.float32))
 
@@ -46,7 +53,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, spec, n1, n2, r, dist, nystrom, q):
+def _worker(rank, world, port, spec, n1, n2, r, dist, nystrom, q, variant="noredist"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,7 +64,7 @@ def _worker(rank, world, port, spec, n1, n2, r, dist, nystrom, q):
         r0, r1, c0, c1 = ds.a_block_range()
         Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1]))
         if nystrom:
-            Bp, (a, b), C = ds.nystrom_core(Ablk)
+            Bp, (a, b), C = ds.nystrom_core_redist(Ablk) if variant == "redist" else ds.nystrom_core(Ablk)
             q.put((rank, a, b, Bp.numpy(), C.numpy(), ds.comm_bytes))
         else:
             Bp, (a, b) = ds.apply(Ablk)
@@ -66,14 +73,15 @@ def _worker(rank, world, port, spec, n1, n2, r, dist, nystrom, q):
         tdist.destroy_process_group()
 
 
-def _run(world, spec, n1, n2, r, dist, nystrom):
+def _run(world, spec, n1, n2, r, dist, nystrom, variant="noredist"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(i, world, port, spec, n1, n2, r, dist, nystrom, q)) for i in range(world)]
+    procs = [ctx.Process(target=_worker, args=(i, world, port, spec, n1, n2, r, dist, nystrom, q, variant))
+             for i in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=180) for _ in range(world)]
+    res = [q.get(timeout=90) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -122,3 +130,18 @@ def test_balanced_split_alignment():
     assert b[0] == 0 and b[-1] == 50000 and all(x % 128 == 0 for x in b[1:-1])
     assert max(b[i + 1] - b[i] for i in range(4)) - min(b[i + 1] - b[i] for i in range(4)) <= 128
     assert balanced_split(10, 3) == [0, 3, 6, 10]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_redist_variant_matches_noredist(world):
+    """Redist (All-to-All of B, column blocks of C) returns the same exact B and C as
+    the No-Redist variant in the integer regime, with the predicted All-to-All + all-gather bytes."""
+    n, r = 520, 24
+    res = _run(world, "row", n, n, r, "rademacher", True, "redist")
+    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+    Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
+    for rank, a, b, Bp, C, comm in res:
+        assert np.array_equal(Bp.astype(np.float64), Bref[a:b])
+        assert np.array_equal(C.astype(np.float64), Cref)
+        pred = predicted_bytes_per_rank(n, r, Layout(world, 1), True, "redist")
+        assert comm == pred

@@ -365,3 +365,18 @@ def test_nystrom_error_decreases_with_rank_gpu():
         B, C = s.nystrom_core(Ad)
         errs.append(quality.reconstruction_error(Ad, B, C))
     assert errs[0] > errs[1] > errs[2]
+
+
+@pytest.mark.parametrize("core", ["auto", "simt"])
+@pytest.mark.parametrize("nb", [1, 7, 64, 100])
+def test_core_block_cols(nb, core):
+    """Column-block core for the Redist variant: C[:, cols] = Omega^T B[:, cols] (all r rows of C)."""
+    sk = _sk()
+    r = 128
+    Bm = synth.int_matrix(17, 3000, nb, -8, 8)
+    s = sk.Sketch(SEED, "rademacher", 5000, r, mode="tf32", core=core)
+    Cc = s.core_block_cols(_dev(Bm), 77).cpu().numpy()
+    Bpad = np.zeros((3000, r))
+    Bpad[:, :nb] = Bm
+    ref = oracle.core(SEED, "rademacher", Bpad, i0=77)[:, :nb]
+    assert Cc.shape == (r, nb) and np.array_equal(Cc.astype(np.float64), ref)
