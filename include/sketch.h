@@ -99,9 +99,18 @@ sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg);
 sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt);
 
 /* Performance ablation for measurements only (results are WRONG while set): bit 0 skips the
- * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs.  0 restores
+ * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs, bit 6 skips the
+ * producers' in-smem A conversion (bf16 / tf32x3).  0 restores
  * normal operation. */
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags);
+
+/* Pipeline trace for measurements only: while `dev_buf` is non-NULL, the next sketch GEMM launches
+ * write %globaltimer stamps (ns, uint64) of their pipeline waits for CTAs 0..159 (layout
+ * [cta][event][stage], 8 events x `stages` stages per CTA; events: 0 TMA after empty_a, 1 MMA after
+ * full_a / conv, 2 MMA after full_o, 3 producer after empty_o, 4 producer share written, 5
+ * producer after pfree, 6 relay after full_o, 7 converter done).  The buffer is device (or mapped
+ * pinned host) memory owned by the caller, >= 160 * 8 * stages * 8 bytes.  NULL disables tracing. */
+sk_status_t sketch_set_trace(sk_sketch_t h, uint64_t* dev_buf, int32_t stages);
 
 /* Bytes of device workspace needed by sketch_apply / sketch_apply_block on n1 rows and
  * nystrom_core / core_apply_block (split-K partials of B and per-CTA r x r partials of C).

@@ -24,7 +24,7 @@ _OMEGA = {"accurate": 0, "fast": 1}
 
 EXPORTED_SYMBOLS = (
     "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
-    "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation",
+    "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation", "sketch_set_trace",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
@@ -178,6 +178,11 @@ class Sketch:
     def set_ablation(self, flags: int) -> None:
         """Measurement-only switches (bit 0: no Omega generation, bit 1: no A loads); results wrong."""
         _check(self._lib.sketch_set_ablation(self._h, int(flags)))
+
+    def set_trace(self, buf=None, stages: int = 0) -> None:
+        """Pipeline trace (measurements only): `buf` a CUDA (or pinned host) int64 tensor of >= 1280*stages entries."""
+        ptr = ctypes.c_void_p(buf.data_ptr() if buf is not None else 0)
+        _check(self._lib.sketch_set_trace(self._h, ptr, int(stages)))
 
     # ------------------------------------------------------------------ profiling
     def set_profiling(self, enable: bool = True) -> None:

@@ -31,6 +31,8 @@ struct sk_sketch_s {
     int core_simt;    // 1: force the fp32 SIMT core GEMM (tests / ablation)
     int cl_override;  // 0 auto, 1 never share Omega between CTA pairs, 2 share whenever possible
     uint32_t ablate;  // performance ablations (bench only): see SketchGemmParams::ablate
+    uint64_t* trace = nullptr;  // pipeline trace buffer (diagnostics)
+    int32_t trace_stages = 0;
     int profiling;
     std::mutex prof_mu;
     std::vector<sk_timed_launch> prof;
@@ -136,7 +138,7 @@ struct SketchPlan {
     int cg;            // 1: one CTA per tile; 2: CTA pair (tcgen05 cta_group::2, M = 256)
     int cl;            // 2: clusters of two CTA pairs sharing every generated Omega slice
     int nacc;
-    int a_stages, o_stages;
+    int a_stages, o_stages, y_stages;
     int split;
     int kiters;
     int num_mblk;
@@ -175,15 +177,20 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     if (bf && P.cg == 2) { a_cap = 3; P.o_stages = 8; }  // bf16 pairs: 3 x 64 KB A, rest Omega ring
     if (const char* e = getenv("SK_A_STAGES")) a_cap = std::max(1, std::min(8, atoi(e)));    // tuning
     if (const char* e = getenv("SK_O_STAGES")) P.o_stages = std::max(1, std::min(8, atoi(e)));  // tuning
+    // bf16: the second fp32 K half of each A stage lives in its own short ring (freed once converted)
+    P.y_stages = bf ? 2 : 0;
+    if (const char* e = getenv("SK_Y_STAGES")) if (bf) P.y_stages = std::max(1, std::min(8, atoi(e)));  // tuning
     for (;;) {
-        const int a_stage = P.nacc * 128 * ks * 4;
-        P.a_stages = std::min(a_cap, (budget - 2 * ostage_bytes(P.nacc)) / a_stage);
-        P.o_stages = std::max(2, std::min(P.o_stages, (budget - P.a_stages * a_stage) / ostage_bytes(P.nacc)));
+        const int a_slot = P.nacc * 128 * (bf ? 32 : ks) * 4;  // bytes of one A-ring slot
+        const int y_bytes = P.y_stages * P.nacc * 128 * 32 * 4;
+        P.a_stages = std::min(a_cap, (budget - y_bytes - 2 * ostage_bytes(P.nacc)) / a_slot);
+        P.o_stages = std::max(2, std::min(P.o_stages, (budget - y_bytes - P.a_stages * a_slot) / ostage_bytes(P.nacc)));
         if (P.a_stages >= 2 || P.nacc == 1) break;
         P.nacc = 1;  // make room for >= 2 A stages
     }
-    const int a_stage = P.nacc * 128 * ks * 4;
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo);
+    const int a_stage = P.nacc * 128 * ks * 4;  // A bytes per K step
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo,
+                                        P.y_stages);
     P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
     // Clusters of two CTA pairs share each generated Omega slice (1024 rows of A per element).
     // Automatic only in bf16 mode, whose 64-wide K steps amortise the extra cross-pair handshake
@@ -236,6 +243,10 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
     P.grid = static_cast<int>(std::min<int64_t>(units, nsm)) * P.cg * P.cl;
     if ((h->ablate & 8u) && (P.grid & 1)) P.grid += 1;  // cluster-of-2 ablation needs an even grid
+    if (getenv("SK_DEBUG_PLAN"))  // tuning diagnostics
+        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d a=%d y=%d o=%d split=%d kiters=%d mblk=%d grid=%d smem=%zu\n",
+                static_cast<long long>(n1), static_cast<long long>(k), P.cg, P.cl, P.nacc, P.a_stages, P.y_stages,
+                P.o_stages, P.split, P.kiters, P.num_mblk, P.grid, P.smem);
     return P;
 }
 
@@ -328,9 +339,16 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.kper = (P.kiters + P.split - 1) / P.split;
         p.a_stages = P.a_stages;
         p.o_stages = P.o_stages;
+        p.y_stages = P.y_stages;
         p.key0 = static_cast<uint32_t>(h->seed);
         p.key1 = static_cast<uint32_t>(h->seed >> 32);
+        for (int i = 0; i < 10; ++i) {
+            p.rk[2 * i] = p.key0 + static_cast<uint32_t>(i) * 0x9E3779B9u;
+            p.rk[2 * i + 1] = p.key1 + static_cast<uint32_t>(i) * 0xBB67AE85u;
+        }
         p.ablate = h->ablate;
+        p.trace = h->trace;
+        p.trace_stages = h->trace_stages;
         if (P.split > 1) {
             p.out = static_cast<float*>(ws);
             p.ldo = p.npad;
@@ -563,7 +581,15 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt) {
 
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    h->ablate = flags & 63u;
+    h->ablate = flags & 127u;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_set_trace(sk_sketch_t h, uint64_t* dev_buf, int32_t stages) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (dev_buf && stages <= 0) return fail(SK_ERR_INVALID_VALUE, "trace needs stages > 0");
+    h->trace = dev_buf;
+    h->trace_stages = dev_buf ? stages : 0;
     return SK_SUCCESS;
 }
 
