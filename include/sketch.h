@@ -100,11 +100,14 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt);
 
 /* Performance ablation for measurements only (results are WRONG while set): bit 0 skips the
  * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs, bit 6 skips the
- * producers' in-smem A conversion (bf16 / tf32x3).  0 restores
+ * producers' in-smem A conversion (bf16 / tf32x3), bit 7 lets one producer warp poll the
+ * stage barriers and release the others with a named barrier, bit 8 makes every bf16 converter
+ * warp poll its A barrier.  0 restores
  * normal operation. */
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags);
 
-/* Pipeline trace for measurements only: while `dev_buf` is non-NULL, the next sketch GEMM launches
+/* Pipeline trace for measurements only (libraries built with SK_BUILD_TRACE=1; otherwise a non-NULL
+ * buffer returns SK_ERR_UNSUPPORTED): while `dev_buf` is non-NULL, the next sketch GEMM launches
  * write %globaltimer stamps (ns, uint64) of their pipeline waits for CTAs 0..159 (layout
  * [cta][event][stage], 8 events x `stages` stages per CTA; events: 0 TMA after empty_a, 1 MMA after
  * full_a / conv, 2 MMA after full_o, 3 producer after empty_o, 4 producer share written, 5

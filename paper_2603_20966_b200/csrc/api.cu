@@ -581,13 +581,16 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt) {
 
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    h->ablate = flags & 127u;
+    h->ablate = flags & 511u;
     return SK_SUCCESS;
 }
 
 sk_status_t sketch_set_trace(sk_sketch_t h, uint64_t* dev_buf, int32_t stages) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
     if (dev_buf && stages <= 0) return fail(SK_ERR_INVALID_VALUE, "trace needs stages > 0");
+#ifndef SK_TRACE
+    if (dev_buf) return fail(SK_ERR_UNSUPPORTED, "library built without SK_TRACE (SK_BUILD_TRACE=1)");
+#endif
     h->trace = dev_buf;
     h->trace_stages = dev_buf ? stages : 0;
     return SK_SUCCESS;

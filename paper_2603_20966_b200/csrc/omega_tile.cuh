@@ -42,11 +42,6 @@ struct TileSink {
         for (int i = 0; i < NR; ++i) r.rbase[i] += d;
         return r;
     }
-    __device__ __forceinline__ void put2(uint32_t off, uint32_t a, uint32_t b) const {
-        asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(base + off), "r"(a), "r"(b) : "memory");
-#pragma unroll
-        for (int i = 0; i < NR; ++i) st_async_v2(rbase[i] + off, a, b, rbar[i]);
-    }
 };
 __device__ __forceinline__ TileSink<0> local_sink(const void* tile) { return TileSink<0>{smem_u32(tile), {0u}, {0u}}; }
 
@@ -205,44 +200,28 @@ __device__ __forceinline__ void produce_omega_tile_bf16_r(const TileSink<NR>& si
 }
 
 // Items of 8 K-values (two Philox calls, one 16-B chunk) dealt as n = c % npad, j8 = c / npad.
-// HALF: items of 4 K-values (one call, 8 B) so that small tiles (npad * 8 < producers) still
-// occupy every producer thread.
-template <int DIST, bool FAST, bool HALF, int NR, class K>
+// (Items of one call, 8 B, keep more threads busy on small tiles but were measured slower: twice
+// the stores, and st.async of 8 B to the cluster partners is expensive.)
+template <int DIST, bool FAST, int NR, class K>
 __device__ __forceinline__ void produce_omega_tile_bf16_g(const TileSink<NR>& sink, int64_t kglob0, int roff,
                                                           int npad, int c0, K key, int n_start, int j_start,
                                                           int tq, int tr) {
     const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;  // call holding row kglob0 - roff
     int n = n_start, j = j_start;
-    constexpr int kJ = HALF ? 16 : 8;
 #pragma unroll 1
-    while (j < kJ) {
+    while (j < 8) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
-        const uint32_t rowoff = static_cast<uint32_t>(n) * 128u;
-        const uint32_t sw = static_cast<uint32_t>(n & 7);
-        if constexpr (HALF) {
-            const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + j, col, key));
-            float v[4] = {a.x, a.y, a.z, a.w};
-            if (roff != 0) {
-                const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + j + 1, col, key));
-                const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j, col, key));
+        const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 1, col, key));
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        if (roff != 0) {
+            const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 2, col, key));
+            const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
-            }
-            sink.put2(rowoff + (((static_cast<uint32_t>(j) >> 1) ^ sw) << 4) + (static_cast<uint32_t>(j) & 1u) * 8u,
-                      pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
-        } else {
-            const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j, col, key));
-            const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 1, col, key));
-            float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            if (roff != 0) {
-                const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 2, col, key));
-                const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
-            }
-            sink.put4(rowoff + ((static_cast<uint32_t>(j) ^ sw) << 4), pack_bf16x2(v[0], v[1]),
-                      pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+            for (int e = 0; e < 8; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
         }
+        sink.put4(static_cast<uint32_t>(n) * 128u + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(n & 7)) << 4),
+                  pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
         n += tr;
         j += tq;
         if (n >= npad) { n -= npad; ++j; }

@@ -398,11 +398,3 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 }  // namespace sk
 
-namespace sk {
-__device__ __forceinline__ void st_async_v2(uint32_t dst_cluster, uint32_t a, uint32_t b, uint32_t bar_cluster) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(
-                     dst_cluster),
-                 "r"(a), "r"(b), "r"(bar_cluster)
-                 : "memory");
-}
-}  // namespace sk

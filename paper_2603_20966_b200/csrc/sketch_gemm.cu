@@ -18,6 +18,8 @@
 //               Warps 4-7 also run the epilogue (tcgen05.ld 32x32b -> st.global of B or of a
 //               split-K partial).
 // Work unit = (m-block of 128*CG*NACC rows, K split s); units are dealt round-robin to CTA groups.
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "omega_tile.cuh"
 #include "philox.cuh"
@@ -32,13 +34,25 @@ constexpr int kCvtWarps = 4;  // bf16: warps converting the fp32 A stage to bf16
 constexpr int threads_for(int mode) { return (kCtlWarps + kRngWarps + (mode == kBF16 ? kCvtWarps : 0)) * 32; }
 constexpr int kRngThreads = kRngWarps * 32;
 
+template <class K>
+__device__ __forceinline__ K make_key(const SketchGemmParams& p) {
+    if constexpr (std::is_same_v<K, PhiloxKeyTable>) return PhiloxKeyTable{p.rk};
+    else return PhiloxKey{p.key0, p.key1};
+}
+
 // diagnostics (sketch_set_trace): %globaltimer stamp of pipeline event `ev` at stage `i`
+// (compiled in only with -DSK_TRACE: even a predicated-off check slows the single-thread TMA / MMA
+// loops measurably)
 __device__ __forceinline__ void trace_stamp(const SketchGemmParams& p, int ev, uint32_t i) {
+#ifdef SK_TRACE
     if (p.trace != nullptr && blockIdx.x < 160u && i < static_cast<uint32_t>(p.trace_stages)) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[(blockIdx.x * 8u + ev) * static_cast<uint32_t>(p.trace_stages) + i] = t;
     }
+#else
+    (void)p; (void)ev; (void)i;
+#endif
 }
 constexpr uint32_t kATileBytes = 128 * 32 * 4;  // one 128-row x 32-fp32 TMA box
 constexpr int kMaxStages = 8;
@@ -330,15 +344,26 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
         uint32_t so = 0, po = 0, sa = 0, pa = 0, local = 0, ntr = 0;
         const uint32_t lo_off = L.olo_off - L.ohi_off;
-        const bool half_items = gen_rows * 8 < kRngThreads;  // bf16: 4-K items keep every thread busy
         // bytes of Omega the partner pairs push into this CTA's stage (CL > 1)
         const uint32_t tx_in = static_cast<uint32_t>(gen_rows) * 128u * (OLO ? 2u : 1u) * NSUBO * (CL - 1);
         for (int u = group; u < total_units; u += ngroups, ++local) {
             const int mb = u / p.split, s = u - (u / p.split) * p.split;
             const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
             for (int kit = kb; kit < ke; ++kit, ++ntr) {
-                if (p.ablate & 32u) mbar_wait(&empty_o[so], po ^ 1);
-                else mbar_wait_sleep(&empty_o[so], po ^ 1);
+                // every producer warp waits on the stage barriers itself (suspend-hinted try_wait).
+                // Bit 7 of the ablation mask: one warp polls and a named barrier releases the others
+                // (fewer polling issue slots, but measured 7% slower at c2: the warps lose their
+                // drift and start every stage together)
+                const bool poll_all = (p.ablate & 128u) == 0;
+                if (poll_all || t < 32) {
+                    if (p.ablate & 32u) mbar_wait(&empty_o[so], po ^ 1);
+                    else mbar_wait_sleep(&empty_o[so], po ^ 1);
+                    if constexpr (CL > 1) {
+                        if (p.ablate & 32u) mbar_wait(&pfree[so], po ^ 1);
+                        else mbar_wait_sleep(&pfree[so], po ^ 1);
+                    }
+                }
+                if (!poll_all) asm volatile("bar.sync 1, %0;" ::"n"(kRngThreads) : "memory");
                 if (t == 0) trace_stamp(p, 3, ntr);
                 uint8_t* ostage = sO + so * L.o_stage;
                 uint8_t* otile = ostage + L.ohi_off + gen_row0 * 128;  // this CTA's generated rows
@@ -347,8 +372,6 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 TileSink<CL - 1> sink;
                 sink.base = smem_u32(otile);
                 if constexpr (CL > 1) {
-                    if (p.ablate & 32u) mbar_wait(&pfree[so], po ^ 1);
-                    else mbar_wait_sleep(&pfree[so], po ^ 1);
                     if (t == 0) trace_stamp(p, 5, ntr);
 #pragma unroll
                     for (int pp = 1; pp < CL; ++pp) {
@@ -357,7 +380,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                         sink.rbar[pp - 1] = mapa_shared(smem_u32(&full_o[so]), partner);
                     }
                 }
-                const PhiloxKeyTable key{p.rk};
+                // Philox round keys: the host-computed table (uniform registers) measured faster
+                // for bf16 / accurate, keys bumped in registers faster for the other modes
+                using KeyT = std::conditional_t<BF && !FAST, PhiloxKeyTable, PhiloxKey>;
+                const KeyT key = make_key<KeyT>(p);
                 if (p.ablate & 1u) {
                     // ablation: stage marked full without generating Omega.  CL > 1 still pushes the
                     // share's bytes (zeros): they are what keeps the pairs of a cluster in lockstep
@@ -373,14 +399,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     if constexpr (DIST == kRademacher)
                         produce_omega_tile_bf16_r<DIST, FAST>(sink, p.k0a + static_cast<int64_t>(kit) * KS,
                                                               p.roff, gen_rows, c0_loc, key, t);
-                    else if (half_items)
-                        produce_omega_tile_bf16_g<DIST, FAST, true>(sink, p.k0a + static_cast<int64_t>(kit) * KS,
-                                                                    p.roff, gen_rows, c0_loc, key,
-                                                                    n_start, j_start, tq, tr);
                     else
-                        produce_omega_tile_bf16_g<DIST, FAST, false>(sink, p.k0a + static_cast<int64_t>(kit) * KS,
-                                                                     p.roff, gen_rows, c0_loc, key,
-                                                                     n_start, j_start, tq, tr);
+                        produce_omega_tile_bf16_g<DIST, FAST>(sink, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                              p.roff, gen_rows, c0_loc, key,
+                                                              n_start, j_start, tq, tr);
                 } else if constexpr (DIST == kRademacher)
                     for (int sb = 0; sb < NSUBO; ++sb)
                         produce_omega_tile_r<DIST, MODE, FAST>(sink.shifted(sb * osub),
@@ -496,7 +518,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             const int s = u - (u / p.split) * p.split;
             const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
             for (int kit = kb; kit < ke; ++kit, ++ntr) {
-                mbar_wait(&full_a[sa], pa);
+                // converter warp 0 polls, a named barrier releases the other converter warps
+                if (p.ablate & 256u) {
+                    mbar_wait(&full_a[sa], pa);
+                } else {
+                    if (cw == 0) mbar_wait(&full_a[sa], pa);
+                    asm volatile("bar.sync 2, %0;" ::"n"(kCvtWarps * 32) : "memory");
+                }
                 if (!(p.ablate & 64u)) {
                     const uint32_t st0 = smem_u32(sA + sa * L.a_stage);
                     const uint32_t y0 = smem_u32(sY + ys * L.y_stage);
