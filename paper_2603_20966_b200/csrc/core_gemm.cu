@@ -238,10 +238,10 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             mbar_wait(&empty_op[so], po ^ 1);
             uint8_t* o_tile = sO + so * L.o_stage;
             if constexpr (DIST == kRademacher)
-                produce_omega_tile_r<DIST, MODE, FAST>(local_sink(o_tile), g0 + 32 * t, 0, nrows, 0, PhiloxKey{p.key0, p.key1}, tt);
+                produce_omega_tile_r<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, 0, p.key0, p.key1, tt);
             else
-                produce_omega_tile_g<DIST, MODE, FAST>(local_sink(o_tile), g0 + 32 * t, 0, nrows, 0,
-                                                       PhiloxKey{p.key0, p.key1}, n_start, j_start, tq, tr);
+                produce_omega_tile_g<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, 0, p.key0, p.key1,
+                                                       n_start, j_start, tq, tr);
             // transpose the raw B tile (32 rows i x npad cols b, 128-B rows per 32-col group) into
             // the K-major SW128 tile: row b, chunk j4 = rows 4 j4 .. 4 j4 + 3
             mbar_wait(&full_raw[sr], pr);

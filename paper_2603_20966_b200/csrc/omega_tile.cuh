@@ -22,41 +22,17 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, float4 v) {
                  : "memory");
 }
 
-// Destination of a generated tile: this CTA's shared memory and, with Omega sharing inside a
-// cluster (sketch GEMM, CL > 1), the same offset in NR partner CTAs through st.async, whose bytes
-// complete on the partner's full barrier.  `off` is relative to the tile's row 0.
-template <int NR>
-struct TileSink {
-    uint32_t base;                   // local shared address of tile row 0
-    uint32_t rbase[NR > 0 ? NR : 1];  // shared::cluster address of the tile in partner CTAs
-    uint32_t rbar[NR > 0 ? NR : 1];   // shared::cluster address of the partner's full barrier
-    __device__ __forceinline__ void put4(uint32_t off, uint32_t a, uint32_t b, uint32_t c, uint32_t d) const {
-        st_shared_v4_u32(base + off, a, b, c, d);
-#pragma unroll
-        for (int i = 0; i < NR; ++i) st_async_v4(rbase[i] + off, a, b, c, d, rbar[i]);
-    }
-    __device__ __forceinline__ TileSink shifted(uint32_t d) const {
-        TileSink r = *this;
-        r.base += d;
-#pragma unroll
-        for (int i = 0; i < NR; ++i) r.rbase[i] += d;
-        return r;
-    }
-};
-__device__ __forceinline__ TileSink<0> local_sink(const void* tile) { return TileSink<0>{smem_u32(tile), {0u}, {0u}}; }
-
-// tf32 mode: Omega rounded RN to tf32.  tf32x3 mode: Omega_hi = tf32_rn(w) at off and
-// Omega_lo = w - Omega_hi (exact in fp32) at off + lo_off (Rademacher: +-1 is exact, no lo tile).
-template <int DIST, int MODE, bool FAST, int NR>
-__device__ __forceinline__ void store_chunk(const TileSink<NR>& sink, uint32_t off, float4 v, uint32_t lo_off = 0) {
+// tf32 mode: Omega rounded RN to tf32.  tf32x3 mode: Omega_hi = tf32_rn(w) at addr and
+// Omega_lo = w - Omega_hi (exact in fp32) at addr + lo_off (Rademacher: +-1 is exact, no lo tile).
+template <int DIST, int MODE, bool FAST>
+__device__ __forceinline__ void store_chunk(uint32_t addr, float4 v, uint32_t lo_off = 0) {
     if constexpr (MODE == kTF32 || MODE == kTF32x3) {
         const float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
-        sink.put4(off, __float_as_uint(h.x), __float_as_uint(h.y), __float_as_uint(h.z), __float_as_uint(h.w));
+        st_shared_v4(addr, h);
         if constexpr (MODE == kTF32x3 && DIST != kRademacher)
-            sink.put4(off + lo_off, __float_as_uint(v.x - h.x), __float_as_uint(v.y - h.y),
-                      __float_as_uint(v.z - h.z), __float_as_uint(v.w - h.w));
+            st_shared_v4(addr + lo_off, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
     } else {
-        sink.put4(off, __float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z), __float_as_uint(v.w));
+        st_shared_v4(addr, v);
     }
 }
 
@@ -74,22 +50,23 @@ __device__ __forceinline__ uint32_t pick_word(uint4 x, uint32_t sel) {
 }
 
 // Rademacher tile: one Philox call per column n = t serves all 32 K-values of the tile.
-template <int DIST, int MODE, bool FAST, int NR, class K>
-__device__ __forceinline__ void produce_omega_tile_r(const TileSink<NR>& sink, int64_t kglob0, int roff,
-                                                     int npad, int c0, K key, int t, uint32_t lo_off = 0) {
+template <int DIST, int MODE, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_r(uint8_t* tile, int64_t kglob0, int roff,
+                                                     int npad, int c0, uint32_t key0,
+                                                     uint32_t key1, int t, uint32_t lo_off = 0) {
     if (t >= npad) return;
     const int n = t;
     const uint32_t col = static_cast<uint32_t>(c0 + n);
-    const uint32_t row_base = static_cast<uint32_t>(n) * 128u;
+    const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
     const uint32_t sw = static_cast<uint32_t>(n & 7);
     {
         // bits for tile rows kk = 0..31: global rows kglob0 + kk
         const uint64_t g = static_cast<uint64_t>(kglob0);
-        const uint4 x = philox_rade_call(g >> 7, col, key);
+        const uint4 x = philox_rade_call(g >> 7, col, key0, key1);
         uint32_t w = pick_word(x, static_cast<uint32_t>(g >> 5) & 3u);
         if (roff != 0) {
             const uint64_t g2 = g + 32;  // next word: same call unless it crosses 128 rows
-            const uint4 x2 = ((g2 >> 7) == (g >> 7)) ? x : philox_rade_call(g2 >> 7, col, key);
+            const uint4 x2 = ((g2 >> 7) == (g >> 7)) ? x : philox_rade_call(g2 >> 7, col, key0, key1);
             const uint32_t w2 = pick_word(x2, static_cast<uint32_t>(g2 >> 5) & 3u);
             w = __funnelshift_r(w, w2, static_cast<uint32_t>(g & 31));
         }
@@ -97,7 +74,7 @@ __device__ __forceinline__ void produce_omega_tile_r(const TileSink<NR>& sink, i
         for (int j4 = 0; j4 < 8; ++j4) {
             const float4 v = make_float4(rade_from_bit(w, 4 * j4 + 0), rade_from_bit(w, 4 * j4 + 1),
                                          rade_from_bit(w, 4 * j4 + 2), rade_from_bit(w, 4 * j4 + 3));
-            store_chunk<DIST, MODE, FAST>(sink, row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v, lo_off);
+            store_chunk<DIST, MODE, FAST>(row_base + ((static_cast<uint32_t>(j4) ^ sw) << 4), v, lo_off);
         }
     }
 }
@@ -105,12 +82,13 @@ __device__ __forceinline__ void produce_omega_tile_r(const TileSink<NR>& sink, i
 // Gaussian / uniform tile: the npad x 8 chunks (one Philox call -> 4 K-values each) are dealt to
 // the kRngThreads producers as c = t + kRngThreads * i, n = c % npad, j4 = c / npad, so a warp
 // stores 32 consecutive rows n at one j4 (conflict-free under the 128-B swizzle).
-template <int DIST, int MODE, bool FAST, int NR, class K>
-__device__ __forceinline__ void produce_omega_tile_g(const TileSink<NR>& sink, int64_t kglob0, int roff,
-                                                     int npad, int c0, K key, int n_start, int j_start,
+template <int DIST, int MODE, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglob0, int roff,
+                                                     int npad, int c0, uint32_t key0,
+                                                     uint32_t key1, int n_start, int j_start,
                                                      int tq, int tr, uint32_t lo_off = 0) {
     const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;
-    const uint32_t tile_base = 0u;
+    const uint32_t tile_base = smem_u32(tile);
     int n = n_start, j4 = j_start;
     if (roff == 0) {
         // two independent chunks per iteration: their Philox / Box-Muller chains interleave
@@ -120,14 +98,14 @@ __device__ __forceinline__ void produce_omega_tile_g(const TileSink<NR>& sink, i
             if (n2 >= npad) { n2 -= npad; ++j2; }
             const bool two = j2 < 8;
             const int n2c = two ? n2 : n, j2c = two ? j2 : j4;
-            const uint4 xa = philox_gauss_call(q0 + j4, static_cast<uint32_t>(c0 + n), key);
-            const uint4 xb = philox_gauss_call(q0 + j2c, static_cast<uint32_t>(c0 + n2c), key);
+            const uint4 xa = philox_gauss_call(q0 + j4, static_cast<uint32_t>(c0 + n), key0, key1);
+            const uint4 xb = philox_gauss_call(q0 + j2c, static_cast<uint32_t>(c0 + n2c), key0, key1);
             const float4 va = values4<DIST, FAST>(xa);
             const float4 vb = values4<DIST, FAST>(xb);
-            store_chunk<DIST, MODE, FAST>(sink, tile_base + static_cast<uint32_t>(n) * 128u +
+            store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n) * 128u +
                                               ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4), va, lo_off);
             if (two)
-                store_chunk<DIST, MODE, FAST>(sink, tile_base + static_cast<uint32_t>(n2) * 128u +
+                store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n2) * 128u +
                                                   ((static_cast<uint32_t>(j2) ^ static_cast<uint32_t>(n2 & 7)) << 4), vb, lo_off);
             n = n2 + tr;
             j4 = j2 + tq;
@@ -138,18 +116,18 @@ __device__ __forceinline__ void produce_omega_tile_g(const TileSink<NR>& sink, i
 #pragma unroll 1
     for (; j4 < 8;) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
-        const uint32_t addr = static_cast<uint32_t>(n) * 128u +
+        const uint32_t addr = tile_base + static_cast<uint32_t>(n) * 128u +
                               ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4);
         // rows 4(q0+j4)+roff .. +3: tail of call q0+j4, head of call q0+j4+1
-        const float4 a0 = values4<DIST, FAST>(philox_gauss_call(q0 + j4, col, key));
-        const float4 a1 = values4<DIST, FAST>(philox_gauss_call(q0 + j4 + 1, col, key));
+        const float4 a0 = values4<DIST, FAST>(philox_gauss_call(q0 + j4, col, key0, key1));
+        const float4 a1 = values4<DIST, FAST>(philox_gauss_call(q0 + j4 + 1, col, key0, key1));
         const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         float4 v;
         v.x = roff == 1 ? a[1] : roff == 2 ? a[2] : a[3];
         v.y = roff == 1 ? a[2] : roff == 2 ? a[3] : a[4];
         v.z = roff == 1 ? a[3] : roff == 2 ? a[4] : a[5];
         v.w = roff == 1 ? a[4] : roff == 2 ? a[5] : a[6];
-        store_chunk<DIST, MODE, FAST>(sink, addr, v, lo_off);
+        store_chunk<DIST, MODE, FAST>(addr, v, lo_off);
         n += tr;
         j4 += tq;
         if (n >= npad) { n -= npad; ++j4; }
@@ -160,25 +138,26 @@ __device__ __forceinline__ void produce_omega_tile_g(const TileSink<NR>& sink, i
 // bf16 tiles: one 64-row K-step, row n (Omega column c0 + n) = 64 bf16 = 128 B, 16-byte chunk
 // j8 (K-values 8 j8 .. 8 j8 + 7) at n*128 + ((j8 ^ (n & 7)) << 4); values rounded RN to bf16.
 // kglob0 = 128-aligned base + 64 * kit + roff.
-template <int DIST, bool FAST, int NR, class K>
-__device__ __forceinline__ void produce_omega_tile_bf16_r(const TileSink<NR>& sink, int64_t kglob0, int roff,
-                                                          int npad, int c0, K key, int t) {
+template <int DIST, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_bf16_r(uint8_t* tile, int64_t kglob0, int roff,
+                                                          int npad, int c0, uint32_t key0,
+                                                          uint32_t key1, int t) {
     (void)roff;
     if (t >= npad) return;
     const int n = t;
     const uint32_t col = static_cast<uint32_t>(c0 + n);
-    const uint32_t row_base = static_cast<uint32_t>(n) * 128u;
+    const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
     const uint32_t sw = static_cast<uint32_t>(n & 7);
     // 64 bits for rows kglob0 .. kglob0 + 63, bit b of the 64 = row kglob0 + b
     const uint64_t g = static_cast<uint64_t>(kglob0);
-    const uint4 x = philox_rade_call(g >> 7, col, key);
+    const uint4 x = philox_rade_call(g >> 7, col, key0, key1);
     const uint32_t sel = static_cast<uint32_t>(g >> 5) & 3u;
     uint32_t w0 = pick_word(x, sel), w1, w2;
     if (sel < 3) {
         w1 = pick_word(x, sel + 1);
-        w2 = (sel < 2) ? pick_word(x, sel + 2) : pick_word(philox_rade_call((g >> 7) + 1, col, key), 0);
+        w2 = (sel < 2) ? pick_word(x, sel + 2) : pick_word(philox_rade_call((g >> 7) + 1, col, key0, key1), 0);
     } else {
-        const uint4 x2 = philox_rade_call((g >> 7) + 1, col, key);
+        const uint4 x2 = philox_rade_call((g >> 7) + 1, col, key0, key1);
         w1 = x2.x;
         w2 = x2.y;
     }
@@ -195,36 +174,37 @@ __device__ __forceinline__ void produce_omega_tile_bf16_r(const TileSink<NR>& si
             const uint32_t s0 = (w >> (b0 + 2 * e)) & 1u, s1 = (w >> (b0 + 2 * e + 1)) & 1u;
             q[e] = (0x3F80u | (s0 << 15)) | ((0x3F80u | (s1 << 15)) << 16);
         }
-        sink.put4(row_base + ((static_cast<uint32_t>(j8) ^ sw) << 4), q[0], q[1], q[2], q[3]);
+        st_shared_v4_u32(row_base + ((static_cast<uint32_t>(j8) ^ sw) << 4), q[0], q[1], q[2], q[3]);
     }
 }
 
-// Items of 8 K-values (two Philox calls, one 16-B chunk) dealt as n = c % npad, j8 = c / npad.
-// (Items of one call, 8 B, keep more threads busy on small tiles but were measured slower: twice
-// the stores, and st.async of 8 B to the cluster partners is expensive.)
-template <int DIST, bool FAST, int NR, class K>
-__device__ __forceinline__ void produce_omega_tile_bf16_g(const TileSink<NR>& sink, int64_t kglob0, int roff,
-                                                          int npad, int c0, K key, int n_start, int j_start,
+template <int DIST, bool FAST>
+__device__ __forceinline__ void produce_omega_tile_bf16_g(uint8_t* tile, int64_t kglob0, int roff,
+                                                          int npad, int c0, uint32_t key0,
+                                                          uint32_t key1, int n_start, int j_start,
                                                           int tq, int tr) {
     const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;  // call holding row kglob0 - roff
-    int n = n_start, j = j_start;
+    const uint32_t tile_base = smem_u32(tile);
+    int n = n_start, j8 = j_start;
 #pragma unroll 1
-    while (j < 8) {
+    while (j8 < 8) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
-        const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j, col, key));
-        const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 1, col, key));
+        const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8, col, key0, key1));
+        const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8 + 1, col, key0, key1));
         float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         if (roff != 0) {
-            const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 2, col, key));
+            const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8 + 2, col, key0, key1));
             const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
         }
-        sink.put4(static_cast<uint32_t>(n) * 128u + ((static_cast<uint32_t>(j) ^ static_cast<uint32_t>(n & 7)) << 4),
-                  pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+        st_shared_v4_u32(tile_base + static_cast<uint32_t>(n) * 128u +
+                             ((static_cast<uint32_t>(j8) ^ static_cast<uint32_t>(n & 7)) << 4),
+                         pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                         pack_bf16x2(v[6], v[7]));
         n += tr;
-        j += tq;
-        if (n >= npad) { n -= npad; ++j; }
+        j8 += tq;
+        if (n >= npad) { n -= npad; ++j8; }
     }
 }
 

@@ -22,50 +22,31 @@ constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
 constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
 constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
 
-// Philox key schedule: round i uses (k0 + i W0, k1 + i W1).  PhiloxKey bumps the key on the fly;
-// PhiloxKeyTable reads the 20 round keys precomputed by the host from kernel parameter space,
-// so every round is 2 IMAD.WIDE + 2 LOP3 with the key as a constant-bank operand.
-struct PhiloxKey {
-    uint32_t k0, k1;
-    __device__ __forceinline__ uint32_t a(int i) const { return k0 + static_cast<uint32_t>(i) * kPhiloxW0; }
-    __device__ __forceinline__ uint32_t b(int i) const { return k1 + static_cast<uint32_t>(i) * kPhiloxW1; }
-};
-struct PhiloxKeyTable {
-    const uint32_t* rk;  // rk[2 i] = k0 + i W0, rk[2 i + 1] = k1 + i W1 (param space)
-    __device__ __forceinline__ uint32_t a(int i) const { return rk[2 * i]; }
-    __device__ __forceinline__ uint32_t b(int i) const { return rk[2 * i + 1]; }
-};
-
-// Philox4x32-10 (Salmon et al. SC'11).
-template <class K>
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, K key) {
+// Philox4x32-10 (Salmon et al. SC'11). The key schedule k + i*W is uniform across the CTA,
+// so the compiler keeps it in uniform registers; each round is 2 IMAD.WIDE + 2 LOP3.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int i = 0; i < 10; ++i) {
         const uint64_t p0 = static_cast<uint64_t>(kPhiloxM0) * c.x;
         const uint64_t p1 = static_cast<uint64_t>(kPhiloxM1) * c.z;
         const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
         const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
-        c = make_uint4(hi1 ^ c.y ^ key.a(i), lo1, hi0 ^ c.w ^ key.b(i), lo0);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
     }
     return c;
 }
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
-    return philox4x32_10(c, PhiloxKey{k0, k1});
-}
 
-template <class K>
-__device__ __forceinline__ uint4 philox_gauss_call(uint64_t q, uint32_t col, K key) {
-    return philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), col, 0u), key);
+__device__ __forceinline__ uint4 philox_gauss_call(uint64_t q, uint32_t col, uint32_t k0,
+                                                   uint32_t k1) {
+    return philox4x32_10(make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), col, 0u),
+                         k0, k1);
 }
-template <class K>
-__device__ __forceinline__ uint4 philox_rade_call(uint64_t g, uint32_t col, K key) {
-    return philox4x32_10(make_uint4(static_cast<uint32_t>(g), static_cast<uint32_t>(g >> 32), col, 1u), key);
-}
-__device__ __forceinline__ uint4 philox_gauss_call(uint64_t q, uint32_t col, uint32_t k0, uint32_t k1) {
-    return philox_gauss_call(q, col, PhiloxKey{k0, k1});
-}
-__device__ __forceinline__ uint4 philox_rade_call(uint64_t g, uint32_t col, uint32_t k0, uint32_t k1) {
-    return philox_rade_call(g, col, PhiloxKey{k0, k1});
+__device__ __forceinline__ uint4 philox_rade_call(uint64_t g, uint32_t col, uint32_t k0,
+                                                  uint32_t k1) {
+    return philox4x32_10(make_uint4(static_cast<uint32_t>(g), static_cast<uint32_t>(g >> 32), col, 1u),
+                         k0, k1);
 }
 
 // ---------------------------------------------------------------------------------------------
