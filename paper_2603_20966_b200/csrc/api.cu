@@ -138,7 +138,7 @@ struct SketchPlan {
     int cg;            // 1: one CTA per tile; 2: CTA pair (tcgen05 cta_group::2, M = 256)
     int cl;            // 2: clusters of two CTA pairs sharing every generated Omega slice
     int nacc;
-    int a_stages, o_stages;
+    int a_stages, o_stages, y_stages;
     int split;
     int kiters;
     int num_mblk;
@@ -177,15 +177,21 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     if (bf && P.cg == 2) { a_cap = 3; P.o_stages = 8; }  // bf16 pairs: 3 x 64 KB A, rest Omega ring
     if (const char* e = getenv("SK_A_STAGES")) a_cap = std::max(1, std::min(8, atoi(e)));    // tuning
     if (const char* e = getenv("SK_O_STAGES")) P.o_stages = std::max(1, std::min(8, atoi(e)));  // tuning
+    // bf16: the second fp32 K half of each A stage lives in a short ring of its own (freed once
+    // converted), so the A ring holds 32 KB slots and the Omega ring gets deeper
+    P.y_stages = bf ? 2 : 0;
+    if (const char* e = getenv("SK_Y_STAGES")) if (bf) P.y_stages = std::max(1, std::min(8, atoi(e)));  // tuning
     for (;;) {
-        const int a_stage = P.nacc * 128 * ks * 4;
-        P.a_stages = std::min(a_cap, (budget - 2 * ostage_bytes(P.nacc)) / a_stage);
-        P.o_stages = std::max(2, std::min(P.o_stages, (budget - P.a_stages * a_stage) / ostage_bytes(P.nacc)));
+        const int a_slot = P.nacc * 128 * (bf ? 32 : ks) * 4;  // bytes of one A-ring slot
+        const int y_bytes = P.y_stages * P.nacc * 128 * 32 * 4;
+        P.a_stages = std::min(a_cap, (budget - y_bytes - 2 * ostage_bytes(P.nacc)) / a_slot);
+        P.o_stages = std::max(2, std::min(P.o_stages, (budget - y_bytes - P.a_stages * a_slot) / ostage_bytes(P.nacc)));
         if (P.a_stages >= 2 || P.nacc == 1) break;
         P.nacc = 1;  // make room for >= 2 A stages
     }
-    const int a_stage = P.nacc * 128 * ks * 4;
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo);
+    const int a_stage = P.nacc * 128 * ks * 4;  // A bytes per K step
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo,
+                                        P.y_stages);
     P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
     // Clusters of CTA pairs share each generated Gaussian Omega slice: every element then feeds
     // 1024 (2 pairs) or 2048 (4 pairs) rows of A instead of 512.  Omega generation is the
@@ -243,8 +249,8 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     P.grid = static_cast<int>(std::min<int64_t>(units, nsm)) * P.cg * P.cl;
     if ((h->ablate & 8u) && (P.grid & 1)) P.grid += 1;  // cluster-of-2 ablation needs an even grid
     if (getenv("SK_DEBUG_PLAN"))  // tuning diagnostics
-        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d a=%d o=%d split=%d kiters=%d mblk=%d grid=%d smem=%zu\n",
-                static_cast<long long>(n1), static_cast<long long>(k), P.cg, P.cl, P.nacc, P.a_stages,
+        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d a=%d y=%d o=%d split=%d kiters=%d mblk=%d grid=%d smem=%zu\n",
+                static_cast<long long>(n1), static_cast<long long>(k), P.cg, P.cl, P.nacc, P.a_stages, P.y_stages,
                 P.o_stages, P.split, P.kiters, P.num_mblk, P.grid, P.smem);
     return P;
 }
@@ -338,6 +344,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.kper = (P.kiters + P.split - 1) / P.split;
         p.a_stages = P.a_stages;
         p.o_stages = P.o_stages;
+        p.y_stages = P.y_stages;
         p.key0 = static_cast<uint32_t>(h->seed);
         p.key1 = static_cast<uint32_t>(h->seed >> 32);
         p.ablate = h->ablate;

@@ -29,6 +29,7 @@ struct SketchGemmParams {
     int32_t kper;         // K iterations per split
     int32_t a_stages;     // A smem pipeline depth
     int32_t o_stages;     // Omega smem pipeline depth
+    int32_t y_stages;     // bf16: depth of the ring holding K 32..63 of each fp32 A stage
     uint32_t key0, key1;  // Philox key = (seed lo, seed hi)
     uint32_t ablate;      // 0 in production; bit 0: skip Omega generation, bit 1: skip A loads
     uint64_t* trace;      // diagnostics (SK_TRACE builds): globaltimer stamps [cta][event][stage]
@@ -81,7 +82,7 @@ cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p
                                cudaStream_t s, int cl = 1);
 int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem);
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa,
-                              bool olo, int ks, int nsubo);
+                              bool olo, int ks, int nsubo, int y_stages);
 int sketch_gemm_max_smem();
 
 cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,

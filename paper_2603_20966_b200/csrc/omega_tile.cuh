@@ -178,33 +178,52 @@ __device__ __forceinline__ void produce_omega_tile_bf16_r(uint8_t* tile, int64_t
     }
 }
 
-template <int DIST, bool FAST>
+// Items of 8 K-values (two Philox calls, one 16-B chunk) dealt as n = c % npad, j8 = c / npad;
+// HALF: items of 4 K-values (one call, 8 B), so that a small tile (npad * 8 items < producer
+// threads, e.g. 32 rows per CTA with clusters of 4 pairs) still keeps every producer busy.
+template <int DIST, bool FAST, bool HALF = false>
 __device__ __forceinline__ void produce_omega_tile_bf16_g(uint8_t* tile, int64_t kglob0, int roff,
                                                           int npad, int c0, uint32_t key0,
                                                           uint32_t key1, int n_start, int j_start,
                                                           int tq, int tr) {
     const uint64_t q0 = static_cast<uint64_t>(kglob0) >> 2;  // call holding row kglob0 - roff
     const uint32_t tile_base = smem_u32(tile);
-    int n = n_start, j8 = j_start;
+    int n = n_start, j = j_start;
+    constexpr int kJ = HALF ? 16 : 8;
 #pragma unroll 1
-    while (j8 < 8) {
+    while (j < kJ) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
-        const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8, col, key0, key1));
-        const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8 + 1, col, key0, key1));
-        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        if (roff != 0) {
-            const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j8 + 2, col, key0, key1));
-            const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+        const uint32_t row = tile_base + static_cast<uint32_t>(n) * 128u;
+        const uint32_t sw = static_cast<uint32_t>(n & 7);
+        if constexpr (HALF) {
+            const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + j, col, key0, key1));
+            float v[4] = {a.x, a.y, a.z, a.w};
+            if (roff != 0) {
+                const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + j + 1, col, key0, key1));
+                const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
+                for (int e = 0; e < 4; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
+            }
+            const uint32_t addr = row + (((static_cast<uint32_t>(j) >> 1) ^ sw) << 4) + (static_cast<uint32_t>(j) & 1u) * 8u;
+            asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(pack_bf16x2(v[0], v[1])),
+                         "r"(pack_bf16x2(v[2], v[3]))
+                         : "memory");
+        } else {
+            const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j, col, key0, key1));
+            const float4 b = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 1, col, key0, key1));
+            float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            if (roff != 0) {
+                const float4 c = values4<DIST, FAST>(philox_gauss_call(q0 + 2 * j + 2, col, key0, key1));
+                const float x[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = roff == 1 ? x[e + 1] : roff == 2 ? x[e + 2] : x[e + 3];
+            }
+            st_shared_v4_u32(row + ((static_cast<uint32_t>(j) ^ sw) << 4), pack_bf16x2(v[0], v[1]),
+                             pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
         }
-        st_shared_v4_u32(tile_base + static_cast<uint32_t>(n) * 128u +
-                             ((static_cast<uint32_t>(j8) ^ static_cast<uint32_t>(n & 7)) << 4),
-                         pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
-                         pack_bf16x2(v[6], v[7]));
         n += tr;
-        j8 += tq;
-        if (n >= npad) { n -= npad; ++j8; }
+        j += tq;
+        if (n >= npad) { n -= npad; ++j; }
     }
 }
 

@@ -28,6 +28,8 @@ namespace sk {
 constexpr int kCtlWarps = 4;
 constexpr int kRngWarps = 16;
 constexpr int kThreads = (kCtlWarps + kRngWarps) * 32;
+constexpr int kCvtWarps = 4;  // bf16: warps converting each fp32 A stage to the bf16 operand
+constexpr int threads_for(int mode) { return (kCtlWarps + kRngWarps + (mode == kBF16 ? kCvtWarps : 0)) * 32; }
 constexpr int kRngThreads = kRngWarps * 32;
 
 // diagnostics (sketch_set_trace, compiled in only with -DSK_TRACE: even a predicated-off check
@@ -49,17 +51,23 @@ constexpr int kMaxStages = 8;
 // Operand ring stage: [A_lo tile (tf32x3 only)] [Omega_hi tile] [Omega_lo tile (tf32x3, Gaussian/uniform)]
 struct SmemLayout {
     uint32_t a_stage, o_stage, a_off, o_off, bar_off, total;
+    uint32_t y_stage, y_off;             // bf16: ring of the second fp32 K half of each A stage
     uint32_t alo_off, ohi_off, olo_off;  // offsets inside an operand stage
 };
 
 // ks: K per pipeline step (32 for tf32 / tf32x3, 64 for bf16: a bf16 swizzle row holds 64 values).
 // xa: the producers write a transformed A operand tile (tf32x3: A_lo fp32; bf16: A in bf16), which
 // takes nacc * 16 KB in the operand stage in both cases.
+// y_stages > 0 (bf16): an A stage's two fp32 boxes per accumulator are split over two rings: box 0
+// (K 0..31) in the A ring, where the converters overwrite it with the bf16 64-K tile the MMA reads,
+// and box 1 (K 32..63) in the Y ring, released as soon as it is converted -- the Y ring only has to
+// cover the conversion, not the MMA, which leaves room for a deeper Omega ring.
 __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stages, int o_stages,
                                                   bool xa = false, bool olo = false, int ks = 32,
-                                                  int nsubo = 1) {
+                                                  int nsubo = 1, int y_stages = 0) {
     SmemLayout L;
-    L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes * static_cast<uint32_t>(ks / 32);
+    L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes * static_cast<uint32_t>(y_stages > 0 ? 1 : ks / 32);
+    L.y_stage = y_stages > 0 ? static_cast<uint32_t>(nacc) * kATileBytes : 0u;
     // nsubo: 32-K sub-tiles per Omega stage (2 for tf32 with 64-wide K steps)
     const uint32_t otile = static_cast<uint32_t>(npad) * 128u * static_cast<uint32_t>(nsubo);
     L.alo_off = 0;
@@ -67,9 +75,10 @@ __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stag
     L.olo_off = L.ohi_off + otile;
     L.o_stage = L.ohi_off + otile * (olo ? 2u : 1u);
     L.a_off = 0;
-    L.o_off = L.a_off + L.a_stage * a_stages;
+    L.y_off = L.a_off + L.a_stage * a_stages;
+    L.o_off = L.y_off + L.y_stage * y_stages;
     L.bar_off = L.o_off + L.o_stage * o_stages;
-    L.total = L.bar_off + (6 * kMaxStages + 4) * 8 + 16;
+    L.total = L.bar_off + (8 * kMaxStages + 4) * 8 + 16;
     return L;
 }
 
@@ -79,7 +88,7 @@ __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stag
 // half into the partner's stage (completing on the partner's full_o), so every generated Omega
 // element feeds 1024 rows of A.  The partner pair's MMA commit multicasts "stage free" (pfree).
 template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_for(MODE), 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
     static_assert(CL == 1 || CG == 2, "Omega sharing between pairs needs CTA pairs");
     static_assert(CL == 1 || CL == 2 || CL == 4, "1, 2 or 4 CTA pairs per cluster");
@@ -99,9 +108,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int KMMA = T64 ? 8 : 4;                      // MMAs (per accumulator) per stage
     const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
     const uint32_t osub = static_cast<uint32_t>(npad_loc) * 128u;  // bytes of one Omega sub-tile
-    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, ALO, OLO, KS, NSUBO);
+    const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, ALO, OLO, KS, NSUBO, BF ? p.y_stages : 0);
     uint8_t* sA = smem + L.a_off;
     uint8_t* sO = smem + L.o_off;
+    uint8_t* sY = smem + L.y_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
     uint64_t* full_a = bars;
     uint64_t* empty_a = bars + kMaxStages;
@@ -109,7 +119,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty_o = bars + 3 * kMaxStages;
     uint64_t* gen_done = bars + 4 * kMaxStages;  // CL = 2: this CTA's Omega half (+ A transform) written
     uint64_t* pfree = bars + 5 * kMaxStages;     // CL = 2: the partner's stage s is free
-    uint64_t* tmem_full = bars + 6 * kMaxStages;
+    uint64_t* conv = bars + 6 * kMaxStages;      // bf16: A stage converted (converter warps)
+    uint64_t* empty_y = bars + 7 * kMaxStages;  // bf16: Y-ring slot converted (free)
+    uint64_t* tmem_full = bars + 8 * kMaxStages;
     uint64_t* tmem_empty = tmem_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 2);
 
@@ -134,7 +146,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (tf32x3 pairs: each CTA's A lands on its own barrier -- its producers read it to form
         // A_lo -- and the peer's completion is relayed to the leader: leader count 2)
         for (int s = 0; s < p.a_stages; ++s) {
-            mbar_init(&full_a[s], 1 + ((ARELAY && leader) ? 1 : 0));
+            mbar_init(&full_a[s], 1 + ((ARELAY && !BF && leader) ? 1 : 0));
+            // bf16: the converter warps' arrivals; the pair leader also counts the peer's relay
+            mbar_init(&conv[s], kCvtWarps + ((CG == 2 && leader) ? 1 : 0));
             mbar_init(&empty_a[s], 1);
         }
         for (int s = 0; s < p.o_stages; ++s) {
@@ -147,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&gen_done[s], kRngWarps);
             mbar_init(&pfree[s], CL > 1 ? CL - 1 : 1);  // one release per partner pair
         }
+        for (int s = 0; s < (BF ? p.y_stages : 0); ++s) mbar_init(&empty_y[s], kCvtWarps);
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, 4 * CG);
         fence_barrier_init();
@@ -170,20 +185,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
             const uint64_t pol = l2_policy_evict_first();
             const uint32_t a_bytes_cta = L.a_stage;
-            uint32_t st = 0, ph = 0, ntr = 0;
+            uint32_t st = 0, ph = 0, ntr = 0, yst = 0, yph = 0;
             for (int u = group; u < total_units; u += ngroups) {
                 const int mb = u / p.split, s = u - (u / p.split) * p.split;
                 const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
                 for (int kit = kb; kit < ke; ++kit) {
                     mbar_wait(&empty_a[st], ph ^ 1);
+                    if constexpr (BF) mbar_wait(&empty_y[yst], yph ^ 1);
                     trace_stamp(p, 0, ntr++);
                     const int x = kit * KS - p.kshift;
                     if (p.ablate & 2u) {  // ablation: no A traffic, stage marked full at once
                         if (leader || ARELAY) mbar_arrive(&full_a[st]);
                         if (++st == static_cast<uint32_t>(p.a_stages)) { st = 0; ph ^= 1; }
+                        if (BF && ++yst == static_cast<uint32_t>(p.y_stages)) { yst = 0; yph ^= 1; }
                         continue;
                     }
-                    if constexpr (CG == 2 && !ARELAY) {
+                    if constexpr (BF) {
+                        // each CTA loads its own rows on its own barrier (its converters read them):
+                        // K 0..31 into the A ring, K 32..63 into the Y ring
+                        mbar_arrive_expect_tx(&full_a[st], 2u * a_bytes_cta);
+#pragma unroll
+                        for (int a = 0; a < NACC; ++a) {
+                            const int row = mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128;
+                            tma_load_2d(sA + st * L.a_stage + a * kATileBytes, &tmA, &full_a[st], x, row, pol);
+                            tma_load_2d(sY + yst * L.y_stage + a * kATileBytes, &tmA, &full_a[st], x + 32, row, pol);
+                        }
+                        if (++yst == static_cast<uint32_t>(p.y_stages)) { yst = 0; yph ^= 1; }
+                    } else if constexpr (CG == 2 && !ARELAY) {
                         // both CTAs load their own rows; bytes are counted on the leader's barrier
                         const uint32_t bar = mapa_shared(smem_u32(&full_a[st]), lead_rank);
                         if (leader) mbar_arrive_expect_tx(&full_a[st], 2 * a_bytes_cta);
@@ -219,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(tmem_empty, (local & 1) ^ 1);
                 tc_fence_after();
                 for (int kit = kb; kit < ke; ++kit, ++ntr) {
-                    mbar_wait(&full_a[sa], pa);
+                    if constexpr (BF) mbar_wait(&conv[sa], pa);  // both CTAs' A stage converted
+                    else mbar_wait(&full_a[sa], pa);
                     trace_stamp(p, 1, ntr);
                     mbar_wait(&full_o[so], po);
                     trace_stamp(p, 2, ntr);
@@ -248,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             if constexpr (BF) {
-                                // bf16 A tile (converted by the producers) in the operand stage
+                                // bf16 A tile (converted in place by the converter warps)
                                 const uint64_t abf = sw128_desc(a_base + a * kATileBytes + k8 * 32, 16, 1024);
                                 if constexpr (CG == 2) mma_bf16_pair(d, abf, bdesc, idesc, acc);
                                 else mma_bf16(d, abf, bdesc, idesc, acc);
@@ -275,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 2 || warp == 3 || (warp == 1 && !leader)) {
         // ------------------------------------------------------------------ relays / copier
-        // Peer CTA: warp 2 forwards its full_o and (XA modes) warp 3 its full_a to the pair leader
+        // Peer CTA: warp 2 forwards its full_o and warp 3 its conv (bf16) / full_a (tf32x3) to the pair leader
         // with a RELAXED cluster-scope arrive (a release.cluster arrive drains in-flight TMA
         // traffic; the relay writes nothing itself).  CL = 2: the copier (leader: warp 3, peer:
         // warp 1) pushes this CTA's Omega half into the partner pair's CTA.
@@ -283,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool is_orelay = (CG == 2) && (CL > 1) && !leader && warp == 2;
         const bool is_arelay = ARELAY && !leader && warp == 3;
         if ((is_copier || is_orelay || is_arelay) && elect_one()) {
-            uint64_t* bars_r = is_orelay ? full_o : full_a;
+            uint64_t* bars_r = is_orelay ? full_o : (BF ? conv : full_a);
             const uint32_t nst = static_cast<uint32_t>(is_arelay ? p.a_stages : p.o_stages);
             const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / CL);
             const uint32_t half_bytes = gen_rows * 128u;  // this CTA's share of one sub-tile
@@ -324,13 +353,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp >= kCtlWarps) {
+    } else if (warp >= kCtlWarps && warp < kCtlWarps + kRngWarps) {
         // ------------------------------------------------------------------ Omega producers + epilogue
         const int t = static_cast<int>(threadIdx.x) - kCtlWarps * 32;
         const int gen_rows = npad_loc / CL;                                      // rows this CTA generates
         const int gen_row0 = static_cast<int>(pairq) * gen_rows;                 // first generated row
-        const int n_start = t % gen_rows, j_start = t / gen_rows;
-        const int tq = kRngThreads / gen_rows, tr = kRngThreads % gen_rows;
+        // tf32 64-K stages hold two 32-K sub-tiles: when one sub-tile has at most half as many
+        // chunks as there are producers (clusters of 4 pairs), each half of the producers takes one
+        // sub-tile instead of both halves idling through the sub-tiles in turn
+        constexpr int kHalfThreads = kRngThreads / 2;
+        const bool split_sub = (NSUBO == 2) && (gen_rows * 8 <= kHalfThreads);
+        const int tt = split_sub ? (t % kHalfThreads) : t;
+        const int my_sub = split_sub ? (t / kHalfThreads) : 0;
+        const int nthr = split_sub ? kHalfThreads : kRngThreads;
+        const int n_start = tt % gen_rows, j_start = tt / gen_rows;
+        const int tq = nthr / gen_rows, tr = nthr % gen_rows;
         const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
         uint32_t so = 0, po = 0, sa = 0, pa = 0, local = 0, ntr = 0;
         const uint32_t lo_off = L.olo_off - L.ohi_off;
@@ -350,57 +387,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                         produce_omega_tile_bf16_r<DIST, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * KS,
                                                               p.roff, gen_rows, c0_loc, p.key0, p.key1, t);
                     else
-                        produce_omega_tile_bf16_g<DIST, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * KS,
-                                                              p.roff, gen_rows, c0_loc, p.key0, p.key1,
-                                                              n_start, j_start, tq, tr);
+                        if (gen_rows * 8 < kRngThreads)  // small share: one-call items
+                            produce_omega_tile_bf16_g<DIST, FAST, true>(otile, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                                  p.roff, gen_rows, c0_loc, p.key0, p.key1,
+                                                                  n_start, j_start, tq, tr);
+                        else
+                            produce_omega_tile_bf16_g<DIST, FAST>(otile, p.k0a + static_cast<int64_t>(kit) * KS,
+                                                                  p.roff, gen_rows, c0_loc, p.key0, p.key1,
+                                                                  n_start, j_start, tq, tr);
                 } else if constexpr (DIST == kRademacher)
                     for (int sb = 0; sb < NSUBO; ++sb)
                         produce_omega_tile_r<DIST, MODE, FAST>(otile + sb * osub,
                                                                p.k0a + static_cast<int64_t>(kit) * KS + 32 * sb,
                                                                p.roff, gen_rows, c0_loc, p.key0, p.key1, t, lo_off);
+                else if (split_sub)
+                    produce_omega_tile_g<DIST, MODE, FAST>(otile + my_sub * osub,
+                                                           p.k0a + static_cast<int64_t>(kit) * KS + 32 * my_sub,
+                                                           p.roff, gen_rows, c0_loc, p.key0, p.key1,
+                                                           n_start, j_start, tq, tr, lo_off);
                 else
                     for (int sb = 0; sb < NSUBO; ++sb)
                         produce_omega_tile_g<DIST, MODE, FAST>(otile + sb * osub,
                                                                p.k0a + static_cast<int64_t>(kit) * KS + 32 * sb,
                                                                p.roff, gen_rows, c0_loc, p.key0, p.key1,
                                                                n_start, j_start, tq, tr, lo_off);
-                if constexpr (BF) {
-                    // A (two fp32 SW128 boxes of 32 K per accumulator) -> one bf16 SW128 tile of 64 K,
-                    // IN PLACE at the start of the A stage (acc a's tile at a * 16 KB): every producer
-                    // first reads its items into registers, a named barrier over the producer warps,
-                    // then the packed bf16 chunks are written.  Item = (acc a, row m, chunk j8 of 8
-                    // K-values); a warp covers 32 consecutive rows (conflict-free under the swizzle).
-                    constexpr int kItems = NACC * 1024 / kRngThreads;
-                    mbar_wait(&full_a[sa], pa);
-                    const uint32_t st0 = smem_u32(sA + sa * L.a_stage);
-                    float4 va[kItems][2];
-#pragma unroll
-                    for (int it = 0; it < kItems; ++it) {
-                        const int i = t + it * kRngThreads;
-                        const int a = i >> 10, rem = i & 1023, m = rem & 127, j8 = rem >> 7;
-                        const uint32_t sw = static_cast<uint32_t>(m & 7);
-                        const uint32_t c0 = 2u * static_cast<uint32_t>(j8 & 3);
-                        const uint32_t row = st0 + static_cast<uint32_t>((a * 2 + (j8 >> 2)) * kATileBytes + m * 128);
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(va[it][0].x), "=f"(va[it][0].y), "=f"(va[it][0].z), "=f"(va[it][0].w)
-                                     : "r"(row + ((c0 ^ sw) << 4)));
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(va[it][1].x), "=f"(va[it][1].y), "=f"(va[it][1].z), "=f"(va[it][1].w)
-                                     : "r"(row + (((c0 + 1) ^ sw) << 4)));
-                    }
-                    asm volatile("bar.sync 1, %0;" ::"n"(kRngThreads) : "memory");  // all reads done
-#pragma unroll
-                    for (int it = 0; it < kItems; ++it) {
-                        const int i = t + it * kRngThreads;
-                        const int a = i >> 10, rem = i & 1023, m = rem & 127, j8 = rem >> 7;
-                        const uint32_t sw = static_cast<uint32_t>(m & 7);
-                        st_shared_v4_u32(st0 + static_cast<uint32_t>(a * kATileBytes + m * 128) +
-                                             ((static_cast<uint32_t>(j8) ^ sw) << 4),
-                                         pack_bf16x2(va[it][0].x, va[it][0].y), pack_bf16x2(va[it][0].z, va[it][0].w),
-                                         pack_bf16x2(va[it][1].x, va[it][1].y), pack_bf16x2(va[it][1].z, va[it][1].w));
-                    }
-                    if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
-                }
                 if constexpr (X3) {
                     // A_lo = A - trunc_tf32(A) (exact), elementwise over this CTA's A tile: the A tile
                     // and A_lo share the SW128 layout, so the copy is layout-agnostic
@@ -476,6 +486,75 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if constexpr (BF) {
+        // ------------------------------------------------------------------ A converters (bf16)
+        // A (two fp32 SW128 boxes of 32 K per accumulator: K 0..31 in the A ring, K 32..63 in the Y
+        // ring) -> one bf16 SW128 tile of 64 K, IN PLACE over the A-ring box.  Row-local: bf16 row m
+        // overwrites only fp32 row m of the A-ring box, so the 8 lanes of one warp that own row m (lane
+        // j8 = 8-K chunk) order their loads before their stores with a __syncwarp.  The two loads
+        // of a lane alternate even / odd chunk so that each 8-lane phase touches 8 distinct 16-B
+        // bank groups; the stores are the 8 distinct chunks of one row.  In their own warps, the
+        // smem-bound conversion overlaps the ALU-bound Omega generation (measured at c2 with
+        // clusters of 4 pairs: the in-producer conversion took ~0.8 of the 1.3 us producer stage).
+        const int cw = static_cast<int>(warp) - (kCtlWarps + kRngWarps);
+        const uint32_t j8 = lane & 7u;
+        const uint32_t hi = j8 >> 2, c0 = 2u * (j8 & 3u);
+        const uint32_t ce = c0 + hi, co = c0 + 1u - hi;  // load order: even chunk first in half 0
+        constexpr int kRowsPerPass = kCvtWarps * 4;        // 4 rows per warp per item
+        constexpr int kUnroll = 4;
+        uint32_t sa = 0, pa = 0, ys = 0;
+        for (int u = group; u < total_units; u += ngroups) {
+            const int s = u - (u / p.split) * p.split;
+            const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+            for (int kit = kb; kit < ke; ++kit) {
+                // converter warp 0 polls, a named barrier releases the other converter warps
+                if (cw == 0) mbar_wait(&full_a[sa], pa);
+                asm volatile("bar.sync 2, %0;" ::"n"(kCvtWarps * 32) : "memory");
+                if (!(p.ablate & 64u)) {
+                    const uint32_t st0 = smem_u32(sA + sa * L.a_stage);
+                    const uint32_t y0 = smem_u32(sY + ys * L.y_stage);
+#pragma unroll 1
+                    for (int r0 = 0; r0 < NACC * 128; r0 += kRowsPerPass * kUnroll) {
+                        uint32_t rowaddr[kUnroll];
+                        float4 va[kUnroll][2];
+#pragma unroll
+                        for (int it = 0; it < kUnroll; ++it) {
+                            const int rr = r0 + it * kRowsPerPass + cw * 4 + static_cast<int>(lane >> 3);
+                            const int a = rr >> 7, m = rr & 127;
+                            const uint32_t sw = static_cast<uint32_t>(m & 7);
+                            const uint32_t roff_b = static_cast<uint32_t>(a * kATileBytes + m * 128);
+                            rowaddr[it] = st0 + roff_b;
+                            const uint32_t src = (hi ? y0 : st0) + roff_b;
+                            float4 x, y;
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                                         : "r"(src + ((ce ^ sw) << 4)));
+                            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                         : "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+                                         : "r"(src + ((co ^ sw) << 4)));
+                            va[it][0] = hi ? y : x;  // K chunk c0
+                            va[it][1] = hi ? x : y;  // K chunk c0 + 1
+                        }
+                        __syncwarp();
+#pragma unroll
+                        for (int it = 0; it < kUnroll; ++it) {
+                            const uint32_t sw = static_cast<uint32_t>((r0 + it * kRowsPerPass + cw * 4 + (lane >> 3)) & 7);
+                            st_shared_v4_u32(rowaddr[it] + ((j8 ^ sw) << 4),
+                                             pack_bf16x2(va[it][0].x, va[it][0].y), pack_bf16x2(va[it][0].z, va[it][0].w),
+                                             pack_bf16x2(va[it][1].x, va[it][1].y), pack_bf16x2(va[it][1].z, va[it][1].w));
+                        }
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty_y[ys]);
+                    mbar_arrive(&conv[sa]);
+                }
+                if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
+                if (++ys == static_cast<uint32_t>(p.y_stages)) ys = 0;
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -488,8 +567,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa, bool olo,
-                              int ks, int nsubo) {
-    return make_layout(nacc, npad / cg, a_stages, o_stages, xa, olo, ks, nsubo).total + 1024;
+                              int ks, int nsubo, int y_stages) {
+    return make_layout(nacc, npad / cg, a_stages, o_stages, xa, olo, ks, nsubo, y_stages).total + 1024;
 }
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
@@ -502,7 +581,7 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
     if (mode >= 0 && mode < 4 && cache[ci][mode][fast ? 1 : 0] > 0) return cache[ci][mode][fast ? 1 : 0] - 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cg * cl * 64);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads_for(mode));
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -545,7 +624,7 @@ static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p,
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads_for(MODE));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
