@@ -26,11 +26,18 @@
 namespace sk {
 
 constexpr int kCtlWarps = 4;
-constexpr int kRngWarps = 16;
+#ifndef SK_RNG_WARPS_BF16
+#define SK_RNG_WARPS_BF16 16
+#endif
+#ifndef SK_CVT_WARPS_BF16
+#define SK_CVT_WARPS_BF16 4
+#endif
+constexpr int kRngWarps = 16;  // Omega producers (the first 4 also run the epilogue)
 constexpr int kThreads = (kCtlWarps + kRngWarps) * 32;
-constexpr int kCvtWarps = 4;  // bf16: warps converting each fp32 A stage to the bf16 operand
-constexpr int threads_for(int mode) { return (kCtlWarps + kRngWarps + (mode == kBF16 ? kCvtWarps : 0)) * 32; }
-constexpr int kRngThreads = kRngWarps * 32;
+// bf16: producer warps and warps converting each fp32 A stage to the bf16 operand
+constexpr int rng_warps(int mode) { return mode == kBF16 ? SK_RNG_WARPS_BF16 : kRngWarps; }
+constexpr int cvt_warps(int mode) { return mode == kBF16 ? SK_CVT_WARPS_BF16 : 0; }
+constexpr int threads_for(int mode) { return (kCtlWarps + rng_warps(mode) + cvt_warps(mode)) * 32; }
 
 // diagnostics (sketch_set_trace, compiled in only with -DSK_TRACE: even a predicated-off check
 // slows the single-thread TMA / MMA loops measurably): %globaltimer stamp of event `ev`, stage `i`
@@ -106,6 +113,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     constexpr int NBOX = KS / 32;                          // 128-B TMA boxes per accumulator
     constexpr int NSUBO = T64 ? 2 : 1;                     // 32-K Omega sub-tiles per stage
     constexpr int KMMA = T64 ? 8 : 4;                      // MMAs (per accumulator) per stage
+    constexpr int kRngW = rng_warps(MODE);                 // Omega producer warps
+    constexpr int kRngThreads = kRngW * 32;
+    constexpr int kCvtWarps = cvt_warps(MODE);             // bf16 converter warps
     const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
     const uint32_t osub = static_cast<uint32_t>(npad_loc) * 128u;  // bytes of one Omega sub-tile
     const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, ALO, OLO, KS, NSUBO, BF ? p.y_stages : 0);
@@ -152,13 +162,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             mbar_init(&empty_a[s], 1);
         }
         for (int s = 0; s < p.o_stages; ++s) {
-            // CL = 1: own kRngWarps warps; CL = 2: the copier's expect_tx arrival (after gen_done),
+            // CL = 1: own kRngW warps; CL = 2: the copier's expect_tx arrival (after gen_done),
             // plus the partner's bulk-copied half as tx bytes.  Leader: + the peer's relayed arrival.
             // CL = 1 pairs: the peer's producer warps arrive directly (relaxed, remote) on the leader
             mbar_init(&full_o[s], (CL > 1) ? (1 + (leader ? 1 : 0))
-                                           : (CG == 2 ? (leader ? 2 * kRngWarps : kRngWarps) : kRngWarps));
+                                           : (CG == 2 ? (leader ? 2 * kRngW : kRngW) : kRngW));
             mbar_init(&empty_o[s], 1);
-            mbar_init(&gen_done[s], kRngWarps);
+            mbar_init(&gen_done[s], kRngW);
             mbar_init(&pfree[s], CL > 1 ? CL - 1 : 1);  // one release per partner pair
         }
         for (int s = 0; s < (BF ? p.y_stages : 0); ++s) mbar_init(&empty_y[s], kCvtWarps);
@@ -353,7 +363,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 }
             }
         }
-    } else if (warp >= kCtlWarps && warp < kCtlWarps + kRngWarps) {
+    } else if (warp >= kCtlWarps && warp < kCtlWarps + kRngW) {
         // ------------------------------------------------------------------ Omega producers + epilogue
         const int t = static_cast<int>(threadIdx.x) - kCtlWarps * 32;
         const int gen_rows = npad_loc / CL;                                      // rows this CTA generates
@@ -496,20 +506,21 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // bank groups; the stores are the 8 distinct chunks of one row.  In their own warps, the
         // smem-bound conversion overlaps the ALU-bound Omega generation (measured at c2 with
         // clusters of 4 pairs: the in-producer conversion took ~0.8 of the 1.3 us producer stage).
-        const int cw = static_cast<int>(warp) - (kCtlWarps + kRngWarps);
+        const int cw = static_cast<int>(warp) - (kCtlWarps + kRngW);
         const uint32_t j8 = lane & 7u;
         const uint32_t hi = j8 >> 2, c0 = 2u * (j8 & 3u);
         const uint32_t ce = c0 + hi, co = c0 + 1u - hi;  // load order: even chunk first in half 0
         constexpr int kRowsPerPass = kCvtWarps * 4;        // 4 rows per warp per item
         constexpr int kUnroll = 4;
-        uint32_t sa = 0, pa = 0, ys = 0;
+        uint32_t sa = 0, pa = 0, ys = 0, ntr = 0;
         for (int u = group; u < total_units; u += ngroups) {
             const int s = u - (u / p.split) * p.split;
             const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
-            for (int kit = kb; kit < ke; ++kit) {
+            for (int kit = kb; kit < ke; ++kit, ++ntr) {
                 // converter warp 0 polls, a named barrier releases the other converter warps
                 if (cw == 0) mbar_wait(&full_a[sa], pa);
                 asm volatile("bar.sync 2, %0;" ::"n"(kCvtWarps * 32) : "memory");
+                if (cw == 0 && lane == 0) trace_stamp(p, 7, ntr);
                 if (!(p.ablate & 64u)) {
                     const uint32_t st0 = smem_u32(sA + sa * L.a_stage);
                     const uint32_t y0 = smem_u32(sY + ys * L.y_stage);

@@ -16,3 +16,8 @@ for f in sys.argv[1:]:
         if c % 2 == 0: msg += f" | mma full_a->full_o {med(e[2,i]-e[1,i]):.0f}  full_o-written {med(e[2,i]-e[4,i]):.0f}  tma->full_a {med(e[1,i]-e[0,i]):.0f}"
         else: msg += f" | relay-written {med(e[6,i]-e[4,i]):.0f}"
         print(msg)
+    if tr[0, 7].max() > 0:
+        for c in (0, 1):
+            e = tr[c]
+            print(f"  cta{c} converter: start-after-tma-issue {med(e[7,i]-e[0,i]):.0f}  period {med(np.diff(e[7,i])):.0f}"
+                  + (f"  conv done (mma full_a) - start {med(tr[0,1,i]-e[7,i]):.0f}" if c == 0 else ""))
