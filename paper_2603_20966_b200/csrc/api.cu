@@ -345,6 +345,8 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.a_stages = P.a_stages;
         p.o_stages = P.o_stages;
         p.y_stages = P.y_stages;
+        p.prefetch = 0;
+        if (const char* e = getenv("SK_PREFETCH")) p.prefetch = std::max(0, std::min(16, atoi(e)));  // tuning
         p.key0 = static_cast<uint32_t>(h->seed);
         p.key1 = static_cast<uint32_t>(h->seed >> 32);
         p.ablate = h->ablate;

@@ -30,6 +30,7 @@ struct SketchGemmParams {
     int32_t a_stages;     // A smem pipeline depth
     int32_t o_stages;     // Omega smem pipeline depth
     int32_t y_stages;     // bf16: depth of the ring holding K 32..63 of each fp32 A stage
+    int32_t prefetch;     // K steps of A prefetched into L2 ahead of the TMA loads (0 = off)
     uint32_t key0, key1;  // Philox key = (seed lo, seed hi)
     uint32_t ablate;      // 0 in production; bit 0: skip Omega generation, bit 1: skip A loads
     uint64_t* trace;      // diagnostics (SK_TRACE builds): globaltimer stamps [cta][event][stage]

@@ -199,10 +199,24 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             for (int u = group; u < total_units; u += ngroups) {
                 const int mb = u / p.split, s = u - (u / p.split) * p.split;
                 const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+                // L2 prefetch of A, p.prefetch K steps ahead of the loads: the HBM latency under load
+                // (~1.6 us) then overlaps the smem ring instead of adding to each stage's turnaround
+                auto prefetch = [&](int kp) {
+                    const int xp = kp * KS - p.kshift;
+#pragma unroll
+                    for (int a = 0; a < NACC; ++a)
+#pragma unroll
+                        for (int bx = 0; bx < NBOX; ++bx)
+                            tma_prefetch_2d(&tmA, xp + 32 * bx,
+                                            mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128);
+                };
+                if (p.prefetch > 0 && !(p.ablate & 2u))
+                    for (int kp = kb; kp < min(kb + p.prefetch, ke); ++kp) prefetch(kp);
                 for (int kit = kb; kit < ke; ++kit) {
                     mbar_wait(&empty_a[st], ph ^ 1);
                     if constexpr (BF) mbar_wait(&empty_y[yst], yph ^ 1);
                     trace_stamp(p, 0, ntr++);
+                    if (p.prefetch > 0 && kit + p.prefetch < ke && !(p.ablate & 2u)) prefetch(kit + p.prefetch);
                     const int x = kit * KS - p.kshift;
                     if (p.ablate & 2u) {  // ablation: no A traffic, stage marked full at once
                         if (leader || ARELAY) mbar_arrive(&full_a[st]);
