@@ -225,6 +225,76 @@ def run_reference(args, W, wl_name):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- f4 ablation
+def omega_ablation(args, W, sk, local, A, ds, dev, world, rank, stream, barrier, reps=5):
+    """SURVEY §8f f4, the B200 version of Fig. 3 (regenerating Omega beats
+    communicating it).  Same A block, B = A * Omega[K_j] only (no core), device time, max over ranks:
+      fused        -- this library: Omega tiles regenerated inside the tcgen05 GEMM (never in HBM);
+      materialise  -- Omega[K_j] generated into HBM by this library's generator kernel, then a cuBLAS
+                      GEMM (torch.matmul; TF32 for tf32 modes; bf16 mode casts A and Omega first);
+      allgather    -- (N > 1) each rank generates 1/N of Omega's rows, all_gather_into_tensor over
+                      NCCL rebuilds Omega[K_j], then the same cuBLAS GEMM.
+    cuBLAS is the comparison system here, not the product path."""
+    import torch
+    import torch.distributed as tdist
+    r0, r1, c0, c1 = ds.a_block_range()
+    k = c1 - c0
+    r = local.r
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev if world > 1 else "cpu")
+        if world > 1:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = args.mode != "tf32x3"
+    out = {"omega_bytes_fp32": 4 * k * r, "a_block": [r1 - r0, k], "reps": reps,
+           "gemm": "torch.matmul (cuBLAS), " + ("bf16 operands" if args.mode == "bf16" else
+                                                  "TF32" if args.mode == "tf32" else "fp32")}
+    Bbuf = torch.empty((r1 - r0, r), dtype=torch.float32, device=dev)
+    out["fused_ms"] = timed(lambda: local.apply_block(A, c0, out=Bbuf))
+    gen_ms = timed(lambda: local.generate(c0, k))
+    Om = local.generate(c0, k)
+    if args.mode == "bf16":
+        gemm = lambda: torch.matmul(A.to(torch.bfloat16), Om.to(torch.bfloat16))
+    else:
+        gemm = lambda: torch.matmul(A, Om)
+    out["materialise_generate_ms"] = gen_ms
+    out["materialise_gemm_ms"] = timed(gemm)
+    out["materialise_ms"] = gen_ms + out["materialise_gemm_ms"]
+    if args.mode == "bf16":  # context: the fp32-operand (TF32) cuBLAS GEMM needs no cast of A
+        torch.backends.cuda.matmul.allow_tf32 = True
+        out["materialise_gemm_tf32_ms"] = timed(lambda: torch.matmul(A, Om))
+    if world > 1:
+        P = world
+        per = -(-k // P)
+        piece_rows = min(per, max(0, k - rank * per))
+        piece = torch.zeros((per, r), dtype=torch.float32, device=dev)
+        full = torch.empty((P * per, r), dtype=torch.float32, device=dev)
+
+        def gather():
+            if piece_rows:
+                piece[:piece_rows].copy_(local.generate(c0 + rank * per, piece_rows))
+            tdist.all_gather_into_tensor(full, piece)
+
+        out["allgather_generate_and_gather_ms"] = timed(gather)
+        out["allgather_ms"] = out["allgather_generate_and_gather_ms"] + out["materialise_gemm_ms"]
+    torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+    del Om
+    return out
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -243,6 +313,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--omega-ablation", action="store_true",
+                    help="f4: also time B = A*Omega with Omega materialised in HBM (+ all-gathered over NCCL "
+                         "when N > 1) and a cuBLAS GEMM, against the fused in-kernel regeneration")
     ap.add_argument("--no-other-modes", action="store_true",
                     help="skip timing the other precision modes / transforms after the main line")
     args = ap.parse_args()
@@ -424,6 +497,10 @@ def main():
             except Exception as e:  # pragma: no cover
                 others[f"{mode}/{omega}"] = {"error": repr(e)}
         result["other_modes"] = others
+
+    # ------------------------------------------------------------------ f4: regenerate vs materialise / gather
+    if args.omega_ablation:
+        result["omega_ablation"] = omega_ablation(args, W, sk, local, A, ds, dev, world, rank, stream, barrier)
 
     # ------------------------------------------------------------------ parity at full size (sampled)
     if rank == 0 and not args.no_parity:
