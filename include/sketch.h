@@ -99,11 +99,10 @@ sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg);
 sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt);
 
 /* Performance ablation for measurements only (results are WRONG while set): bit 0 skips the
- * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs, bit 6 skips the
- * producers' in-smem A conversion (bf16 / tf32x3), bit 7 lets one producer warp poll the
- * stage barriers and release the others with a named barrier, bit 8 makes every bf16 converter
- * warp poll its A barrier.  0 restores
- * normal operation. */
+ * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs, bit 3 runs
+ * single-CTA tiles in clusters of 2, bit 4 uses release (not relaxed) cluster relays, bit 5 makes
+ * the producers spin instead of suspend-waiting, bit 6 skips the converter warps' A transform
+ * (bf16 conversion / tf32x3 A_lo).  0 restores normal operation. */
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags);
 
 /* Pipeline trace for measurements only (libraries built with SK_BUILD_TRACE=1; otherwise a non-NULL

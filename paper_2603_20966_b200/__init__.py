@@ -176,7 +176,7 @@ class Sketch:
             self._h = None
 
     def set_ablation(self, flags: int) -> None:
-        """Measurement-only switches (bit 0: no Omega generation, bit 1: no A loads); results wrong."""
+        """Measurement-only switches (see sketch_set_ablation in include/sketch.h); results are wrong while set."""
         _check(self._lib.sketch_set_ablation(self._h, int(flags)))
 
     def set_trace(self, buf=None, stages: int = 0) -> None:

@@ -166,12 +166,12 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int nsubo = t64 ? 2 : 1;
     const bool olo = x3 && h->dist != sk::kRademacher;
     // Omega ring depth: pairs hand every stage across the pair (relay + multicast commit)
-    P.o_stages = xa ? 2 : ((P.cg == 2) ? 3 : 2);
+    P.o_stages = bf ? 2 : ((P.cg == 2 || x3) ? 3 : 2);
     const int budget = sk::sketch_gemm_max_smem() - 2048;
-    // operand stage: [A_lo (tf32x3)] + Omega (+ Omega_lo); bf16 converts A in place in its A stage
-    auto ostage_bytes = [&](int nacc) {
+    // operand stage: Omega (+ Omega_lo); tf32x3 keeps A_lo in the A stage, bf16 converts A in place
+    auto ostage_bytes = [&](int) {
         const int otile = (npad_max / P.cg) * 128 * nsubo;
-        return (x3 ? nacc * 128 * 32 * 4 : 0) + otile * (olo ? 2 : 1);
+        return otile * (olo ? 2 : 1);
     };
     int a_cap = 6;
     if (bf && P.cg == 2) { a_cap = 3; P.o_stages = 8; }  // bf16 pairs: 3 x 64 KB A, rest Omega ring
@@ -182,7 +182,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     P.y_stages = bf ? 2 : 0;
     if (const char* e = getenv("SK_Y_STAGES")) if (bf) P.y_stages = std::max(1, std::min(8, atoi(e)));  // tuning
     for (;;) {
-        const int a_slot = P.nacc * 128 * (bf ? 32 : ks) * 4;  // bytes of one A-ring slot
+        const int a_slot = P.nacc * 128 * (bf ? 32 : ks) * 4 * (x3 ? 2 : 1);  // bytes of one A-ring slot
         const int y_bytes = P.y_stages * P.nacc * 128 * 32 * 4;
         P.a_stages = std::min(a_cap, (budget - y_bytes - 2 * ostage_bytes(P.nacc)) / a_slot);
         P.o_stages = std::max(2, std::min(P.o_stages, (budget - y_bytes - P.a_stages * a_slot) / ostage_bytes(P.nacc)));
@@ -584,7 +584,7 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt) {
 
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    h->ablate = flags & 511u;
+    h->ablate = flags & 127u;
     return SK_SUCCESS;
 }
 

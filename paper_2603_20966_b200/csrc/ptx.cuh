@@ -387,21 +387,4 @@ __device__ __forceinline__ void epi_store_tile(const CUtensorMap* map, uint8_t* 
 }
 }  // namespace sk
 
-namespace sk {
-// Asynchronous 16-byte store into another CTA's shared memory; completion counted in bytes on that
-// CTA's mbarrier (both shared::cluster addresses).
-__device__ __forceinline__ void st_async_v4(uint32_t dst_cluster, uint32_t a, uint32_t b, uint32_t c,
-                                            uint32_t d, uint32_t bar_cluster) {
-    asm volatile(
-        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-            dst_cluster),
-        "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar_cluster)
-        : "memory");
-}
-// Raise the expected transaction count of a local mbarrier's current phase without arriving.
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-}  // namespace sk
 

@@ -36,7 +36,7 @@ constexpr int kRngWarps = 16;  // Omega producers (the first 4 also run the epil
 constexpr int kThreads = (kCtlWarps + kRngWarps) * 32;
 // bf16: producer warps and warps converting each fp32 A stage to the bf16 operand
 constexpr int rng_warps(int mode) { return mode == kBF16 ? SK_RNG_WARPS_BF16 : kRngWarps; }
-constexpr int cvt_warps(int mode) { return mode == kBF16 ? SK_CVT_WARPS_BF16 : 0; }
+constexpr int cvt_warps(int mode) { return (mode == kBF16 || mode == kTF32x3) ? SK_CVT_WARPS_BF16 : 0; }
 constexpr int threads_for(int mode) { return (kCtlWarps + rng_warps(mode) + cvt_warps(mode)) * 32; }
 
 // diagnostics (sketch_set_trace, compiled in only with -DSK_TRACE: even a predicated-off check
@@ -63,22 +63,23 @@ struct SmemLayout {
 };
 
 // ks: K per pipeline step (32 for tf32 / tf32x3, 64 for bf16: a bf16 swizzle row holds 64 values).
-// xa: the producers write a transformed A operand tile (tf32x3: A_lo fp32; bf16: A in bf16), which
-// takes nacc * 16 KB in the operand stage in both cases.
+// a_lo (tf32x3): each A stage also holds the A_lo = A - trunc_tf32(A) tiles the converter warps
+// write next to the TMA'd A tiles (nacc * 16 KB more per stage).
 // y_stages > 0 (bf16): an A stage's two fp32 boxes per accumulator are split over two rings: box 0
 // (K 0..31) in the A ring, where the converters overwrite it with the bf16 64-K tile the MMA reads,
 // and box 1 (K 32..63) in the Y ring, released as soon as it is converted -- the Y ring only has to
 // cover the conversion, not the MMA, which leaves room for a deeper Omega ring.
 __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stages, int o_stages,
-                                                  bool xa = false, bool olo = false, int ks = 32,
+                                                  bool a_lo = false, bool olo = false, int ks = 32,
                                                   int nsubo = 1, int y_stages = 0) {
     SmemLayout L;
-    L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes * static_cast<uint32_t>(y_stages > 0 ? 1 : ks / 32);
+    L.a_stage = static_cast<uint32_t>(nacc) * kATileBytes * static_cast<uint32_t>(y_stages > 0 ? 1 : ks / 32) *
+                (a_lo ? 2u : 1u);
     L.y_stage = y_stages > 0 ? static_cast<uint32_t>(nacc) * kATileBytes : 0u;
     // nsubo: 32-K sub-tiles per Omega stage (2 for tf32 with 64-wide K steps)
     const uint32_t otile = static_cast<uint32_t>(npad) * 128u * static_cast<uint32_t>(nsubo);
     L.alo_off = 0;
-    L.ohi_off = xa ? static_cast<uint32_t>(nacc) * kATileBytes : 0u;
+    L.ohi_off = 0u;
     L.olo_off = L.ohi_off + otile;
     L.o_stage = L.ohi_off + otile * (olo ? 2u : 1u);
     L.a_off = 0;
@@ -104,8 +105,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                                                ~static_cast<uintptr_t>(1023));
     constexpr bool X3 = (MODE == kTF32x3);                 // 3xTF32: A_lo and Omega_lo operands
     constexpr bool BF = (MODE == kBF16);                   // bf16 operands, K = 16 per MMA
-    constexpr bool XA = X3 || BF;                          // producers transform A in smem
-    constexpr bool ALO = X3;                               // transformed A lives in the operand stage
+    constexpr bool XA = X3 || BF;                          // converter warps transform A in smem
+    constexpr bool ALO = X3;                               // A_lo tiles live in the A stage
     constexpr bool OLO = X3 && (DIST != kRademacher);      // +-1 is exact in tf32: no Omega_lo
     constexpr bool ARELAY = (CG == 2) && XA;               // peer A lands on its own barrier
     constexpr bool T64 = (MODE == kTF32) && (CG == 2);    // tf32 pairs: 64-wide K steps
@@ -156,8 +157,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // (tf32x3 pairs: each CTA's A lands on its own barrier -- its producers read it to form
         // A_lo -- and the peer's completion is relayed to the leader: leader count 2)
         for (int s = 0; s < p.a_stages; ++s) {
-            mbar_init(&full_a[s], 1 + ((ARELAY && !BF && leader) ? 1 : 0));
-            // bf16: the converter warps' arrivals; the pair leader also counts the peer's relay
+            mbar_init(&full_a[s], 1);
+            // bf16 / tf32x3: the converter warps' arrivals; the pair leader also counts the peer's relay
             mbar_init(&conv[s], kCvtWarps + ((CG == 2 && leader) ? 1 : 0));
             mbar_init(&empty_a[s], 1);
         }
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // ------------------------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint64_t pol = l2_policy_evict_first();
-            const uint32_t a_bytes_cta = L.a_stage;
+            const uint32_t a_bytes_cta = ALO ? L.a_stage / 2 : L.a_stage;  // (tf32x3: A_lo not loaded)
             uint32_t st = 0, ph = 0, ntr = 0, yst = 0, yph = 0;
             for (int u = group; u < total_units; u += ngroups) {
                 const int mb = u / p.split, s = u - (u / p.split) * p.split;
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 mbar_wait(tmem_empty, (local & 1) ^ 1);
                 tc_fence_after();
                 for (int kit = kb; kit < ke; ++kit, ++ntr) {
-                    if constexpr (BF) mbar_wait(&conv[sa], pa);  // both CTAs' A stage converted
+                    if constexpr (XA) mbar_wait(&conv[sa], pa);  // both CTAs' A stage converted
                     else mbar_wait(&full_a[sa], pa);
                     trace_stamp(p, 1, ntr);
                     mbar_wait(&full_o[so], po);
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                             const uint32_t d = tmem_base + a * p.npad;
                             if constexpr (X3) {
                                 // small terms first: A_lo * Omega_hi, A_hi * Omega_lo, then A_hi * Omega_hi
-                                const uint64_t alo = sw128_desc(o_base + L.alo_off + a * kATileBytes + k8 * 32, 16, 1024);
+                                const uint64_t alo = sw128_desc(a_base + (NACC + a) * kATileBytes + k8 * 32, 16, 1024);
                                 if constexpr (CG == 2) mma_tf32_pair(d, alo, bdesc, idesc, acc);
                                 else mma_tf32(d, alo, bdesc, idesc, acc);
                                 acc = 1u;
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         const bool is_orelay = (CG == 2) && (CL > 1) && !leader && warp == 2;
         const bool is_arelay = ARELAY && !leader && warp == 3;
         if ((is_copier || is_orelay || is_arelay) && elect_one()) {
-            uint64_t* bars_r = is_orelay ? full_o : (BF ? conv : full_a);
+            uint64_t* bars_r = is_orelay ? full_o : conv;
             const uint32_t nst = static_cast<uint32_t>(is_arelay ? p.a_stages : p.o_stages);
             const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / CL);
             const uint32_t half_bytes = gen_rows * 128u;  // this CTA's share of one sub-tile
@@ -435,22 +436,6 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                                                                p.k0a + static_cast<int64_t>(kit) * KS + 32 * sb,
                                                                p.roff, gen_rows, c0_loc, p.key0, p.key1,
                                                                n_start, j_start, tq, tr, lo_off);
-                if constexpr (X3) {
-                    // A_lo = A - trunc_tf32(A) (exact), elementwise over this CTA's A tile: the A tile
-                    // and A_lo share the SW128 layout, so the copy is layout-agnostic
-                    mbar_wait(&full_a[sa], pa);
-                    const float4* src = reinterpret_cast<const float4*>(sA + sa * L.a_stage);
-                    float4* dst = reinterpret_cast<float4*>(ostage + L.alo_off);
-                    for (int i = t; i < static_cast<int>(L.a_stage / 16); i += kRngThreads) {
-                        float4 v = src[i];
-                        v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                        v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                        v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                        v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                        dst[i] = v;
-                    }
-                    if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
-                }
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (t == 0) trace_stamp(p, 4, ntr);
@@ -508,6 +493,39 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(tmem_empty), lead_rank));
                     else mbar_arrive(tmem_empty);
                 }
+            }
+        }
+    } else if constexpr (X3) {
+        // ------------------------------------------------------------------ A_lo writers (tf32x3)
+        // A_lo = A - trunc_tf32(A) (exact in fp32), elementwise next to the TMA'd A tiles of the same
+        // stage (same SW128 layout, so the copy is layout-agnostic); the MMA reads A (as tf32, i.e.
+        // truncated) and A_lo.  In their own warps this overlaps the Omega generation.
+        const int cw = static_cast<int>(warp) - (kCtlWarps + kRngW);
+        const int ct = cw * 32 + static_cast<int>(lane);
+        uint32_t sa = 0, pa = 0;
+        for (int u = group; u < total_units; u += ngroups) {
+            const int s = u - (u / p.split) * p.split;
+            const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+            for (int kit = kb; kit < ke; ++kit) {
+                if (cw == 0) mbar_wait(&full_a[sa], pa);
+                asm volatile("bar.sync 2, %0;" ::"n"(kCvtWarps * 32) : "memory");
+                if (!(p.ablate & 64u)) {
+                    const float4* src = reinterpret_cast<const float4*>(sA + sa * L.a_stage);
+                    float4* dst = reinterpret_cast<float4*>(sA + sa * L.a_stage + NACC * kATileBytes);
+#pragma unroll 4
+                    for (int i = ct; i < static_cast<int>(NACC * kATileBytes / 16); i += kCvtWarps * 32) {
+                        float4 v = src[i];
+                        v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                        v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                        v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                        v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                        dst[i] = v;
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv[sa]);
+                if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
             }
         }
     } else if constexpr (BF) {
