@@ -313,6 +313,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--fused-rs", action="store_true",
+                    help="f1: column / 2D layouts reduce-scatter partial B from the GEMM epilogue over NVLink "
+                         "(symmetric memory) instead of NCCL reduce_scatter")
     ap.add_argument("--omega-ablation", action="store_true",
                     help="f4: also time B = A*Omega with Omega materialised in HBM (+ all-gathered over NCCL "
                          "when N > 1) and a cuBLAS GEMM, against the fused in-kernel regeneration")
@@ -347,7 +350,7 @@ def main():
     peaks = load_peaks()
 
     local = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=args.mode, omega=args.omega, split_k=args.split_k)
-    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local)
+    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.fused_rs)
     r0, r1, c0, c1 = ds.a_block_range()
     t_gen = time.perf_counter()
     A = make_A_block(W, args.workload, r0, r1, c0, c1, dev)
@@ -457,6 +460,7 @@ def main():
         "host_submit_ms_per_step": host_ms,
         "clocks": clocks,
         "comm": {"variant": args.variant if (W["nystrom"] and world > 1) else None,
+                 "fused_reduce_scatter": bool(ds.fused_rs),
                  "predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"],
                                                                      args.variant if world > 1 else "noredist"),
                  "measured_bytes_per_rank": comm_bytes},

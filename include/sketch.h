@@ -114,6 +114,31 @@ sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags);
  * pinned host) memory owned by the caller, >= 160 * 8 * stages * 8 bytes.  NULL disables tracing. */
 sk_status_t sketch_set_trace(sk_sketch_t h, uint64_t* dev_buf, int32_t stages);
 
+/* Fused reduce-scatter of the partial sketch (Alg. 1, on a
+ * p1 x p2 grid with p2 > 1).  B-bar = A_blk[m x k] * Omega[k0 : k0+k, 0:r] is not formed locally:
+ * the GEMM epilogue stores every row i (0 <= i < m) straight into the receive buffer of the rank
+ * owning row piece i / piece_rows, at
+ *     dst[i / piece_rows] + (slot * split + s) * slot_elems + (i % piece_rows) * npad + c,
+ * s < split the split-K index, npad = round_up(r, 16), c < r.  dst[] holds ndst (<= 8) device
+ * pointers valid in this process -- typically NVLink peer mappings of symmetric-memory receive
+ * buffers, so the reduce-scatter traffic leaves each SM as its tiles finish; slot = this rank's
+ * index in its row group.  split must be equal on all ranks of the group (sketch_rs_split gives the
+ * local choice; take the max over the group).  The owners then call sketch_reduce_slots on their
+ * ndst * split slots after a cross-rank barrier.  Requires r <= 256.  Stream-ordered on `stream`.
+ * Errors: as sketch_apply_block, SK_ERR_INVALID_VALUE (ndst, pieces, slot, split),
+ * SK_ERR_SHAPE_MISMATCH (slot_elems), SK_ERR_ALIGNMENT (dst not 16-byte aligned),
+ * SK_ERR_UNSUPPORTED (r > 256). */
+sk_status_t sketch_rs_split(sk_sketch_t h, int64_t m, int64_t k, int32_t* split);
+sk_status_t sketch_apply_block_rs(sk_sketch_t h, const float* A_blk, int64_t m, int64_t k, int64_t lda,
+                                  int64_t k0, float* const* dst, int32_t ndst, int64_t piece_rows,
+                                  int32_t slot, int64_t slot_elems, int32_t split, void* stream);
+
+/* B[rows x r] (ldb) = sum over s < nslots of slots[s * slot_elems + i * npad + c], summed in increasing
+ * s (fixed order, deterministic): the owner-side half of the fused reduce-scatter.  slots is a device
+ * buffer of nslots * slot_elems floats.  Errors: SK_ERR_INVALID_VALUE, SK_ERR_SHAPE_MISMATCH. */
+sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslots, int64_t slot_elems,
+                                int64_t rows, float* B, int64_t ldb, void* stream);
+
 /* Bytes of device workspace needed by sketch_apply / sketch_apply_block on n1 rows and
  * nystrom_core / core_apply_block (split-K partials of B and per-CTA r x r partials of C).
  * One size covers every entry point for that n1 (n for nystrom_core). */

@@ -27,6 +27,7 @@ EXPORTED_SYMBOLS = (
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation", "sketch_set_trace",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
+    "sketch_rs_split", "sketch_apply_block_rs", "sketch_reduce_slots",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
@@ -81,6 +82,11 @@ def load_library(build_if_missing: bool = True):
         lib.sketch_host_workspace_size.argtypes = [vp, i64, i64, ctypes.POINTER(sz)]
         lib.sketch_apply_host.argtypes = [vp, vp, i64, i64, i64, vp, i64, i64, vp, sz, vp]
         lib.nystrom_core_host.argtypes = [vp, vp, i64, i64, vp, i64, vp, i64, i64, vp, sz, vp]
+        lib.sketch_rs_split.argtypes = [vp, i64, i64, ctypes.POINTER(i32)]
+        lib.sketch_apply_block_rs.argtypes = [vp, vp, i64, i64, i64, i64, ctypes.POINTER(vp), i32, i64, i32, i64,
+                                              i32, vp]
+        lib.sketch_reduce_slots.argtypes = [vp, vp, i32, i64, i64, vp, i64, vp]
+        lib.sketch_set_trace.argtypes = [vp, vp, i32]
         lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_generate_bits.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_debug_box_muller.argtypes = [vp, vp, i64, ctypes.c_int, vp, vp, vp]
@@ -241,6 +247,39 @@ class Sketch:
         _check(self._lib.sketch_apply_block(self._h, A_blk.data_ptr(), m, k, A_blk.stride(0), int(k0),
                                             out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
                                             _stream_ptr(stream)))
+        return out
+
+    # ------------------------------------------------------------------ fused reduce-scatter (f1)
+    def rs_split(self, m: int, k: int) -> int:
+        v = ctypes.c_int32(0)
+        _check(self._lib.sketch_rs_split(self._h, ctypes.c_int64(m), ctypes.c_int64(k), ctypes.byref(v)))
+        return int(v.value)
+
+    def apply_block_rs(self, A_blk, k0: int, dst_ptrs, piece_rows: int, slot: int, slot_elems: int, split: int,
+                       stream=None):
+        """Partial B = A_blk Omega[k0:k0+k] stored by the GEMM epilogue into the owners' receive
+        buffers (device pointers dst_ptrs, e.g. symmetric-memory peers); see sketch_apply_block_rs."""
+        _require_cuda(A_blk)
+        m, k = A_blk.shape
+        A_blk = _tma_ready(A_blk)
+        arr = (ctypes.c_void_p * len(dst_ptrs))(*[ctypes.c_void_p(int(x)) for x in dst_ptrs])
+        _check(self._lib.sketch_apply_block_rs(self._h, ctypes.c_void_p(A_blk.data_ptr()), ctypes.c_int64(m),
+                                               ctypes.c_int64(k), ctypes.c_int64(A_blk.stride(0)),
+                                               ctypes.c_int64(k0), arr, ctypes.c_int32(len(dst_ptrs)),
+                                               ctypes.c_int64(piece_rows), ctypes.c_int32(slot),
+                                               ctypes.c_int64(slot_elems), ctypes.c_int32(split),
+                                               _stream_ptr(stream)))
+
+    def reduce_slots(self, slots, nslots: int, slot_elems: int, rows: int, out=None, stream=None):
+        """out[rows x r] = sum of the nslots receive slots, fixed order (owner side of the fused RS)."""
+        torch = _torch()
+        _require_cuda(slots, out)
+        if out is None:
+            out = torch.empty((rows, self.r), dtype=torch.float32, device=slots.device)
+        _check(self._lib.sketch_reduce_slots(self._h, ctypes.c_void_p(slots.data_ptr()), ctypes.c_int32(nslots),
+                                             ctypes.c_int64(slot_elems), ctypes.c_int64(rows),
+                                             ctypes.c_void_p(out.data_ptr()), ctypes.c_int64(out.stride(0)),
+                                             _stream_ptr(stream)))
         return out
 
     def core_block(self, B_blk, i0: int, out=None, stream=None):

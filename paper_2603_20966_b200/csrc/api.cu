@@ -147,7 +147,8 @@ struct SketchPlan {
     size_t ws_per_split;  // bytes of one split partial (n1 x npad_max)
 };
 
-SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, size_t ws_cap) {
+SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, size_t ws_cap,
+                       int force_split = 0) {
     SketchPlan P{};
     const int64_t rpad = round_up(h->r, 16);
     P.npass = static_cast<int>((rpad + 255) / 256);
@@ -222,7 +223,9 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // partials are summed in fp32 round-to-nearest.
     const int min_split = x3 ? (P.kiters + 31) / 32 : 1;
     int best_s = 1;
-    if (h->split_override > 0) {
+    if (force_split > 0) {
+        best_s = std::min(force_split, std::max(1, P.kiters));
+    } else if (h->split_override > 0) {
         best_s = std::min(h->split_override, std::max(1, P.kiters));
     } else if (min_split > 64) {
         best_s = min_split;
@@ -240,7 +243,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
             if (t < best * 0.995) { best = t; best_s = s; }
         }
     }
-    if (best_s > 1 && ws_cap < static_cast<size_t>(best_s) * P.ws_per_split)
+    if (best_s > 1 && force_split == 0 && ws_cap < static_cast<size_t>(best_s) * P.ws_per_split)
         best_s = std::max<int>(1, static_cast<int>(ws_cap / P.ws_per_split));
     // each split must own >= 1 K iteration
     const int kper = (P.kiters + best_s - 1) / best_s;
@@ -316,15 +319,27 @@ sk_status_t check_mode(const sk_sketch_s* h) {
 }
 
 // B_part[m x r] = A[m x k] * Omega[k0 : k0+k, :r]
+// Fused reduce-scatter target (f1): output rows go to peer receive buffers, see sketch.h
+struct RsTarget {
+    float* dst[8];
+    int32_t ndst;
+    int32_t slot;
+    int64_t piece;
+    int64_t slot_elems;
+    int32_t split;
+};
+
 sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int64_t lda,
                        int64_t k0, float* B, int64_t ldb, void* ws, size_t ws_bytes,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, const RsTarget* rs = nullptr) {
     if (m == 0) return SK_SUCCESS;
     // Omega tile rows start at a 128-aligned global row (+ roff = k0 % 4); the matching A columns
     // start kshift (a multiple of 4) columns left of column 0 and are zero-filled by TMA.
     const int kshift = static_cast<int>(k0 & 124);
     const int roff = static_cast<int>(k0 & 3);
-    const SketchPlan P = plan_sketch(h, m, k, kshift, ws_bytes);
+    const SketchPlan P = plan_sketch(h, m, k, kshift, rs ? ~size_t(0) : ws_bytes, rs ? rs->split : 0);
+    if (rs && (P.npass != 1 || P.split != rs->split))
+        return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256 and split <= K iterations");
     CUtensorMap map;
     sk_status_t st = make_map_2d(&map, A, m, k, lda, 32, 128);
     if (st != SK_SUCCESS) return st;
@@ -352,7 +367,16 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.ablate = h->ablate;
         p.trace = h->trace;
         p.trace_stages = h->trace_stages;
-        if (P.split > 1) {
+        if (rs) {
+            for (int j = 0; j < 8; ++j) p.rs_dst[j] = j < rs->ndst ? rs->dst[j] : nullptr;
+            p.rs_ndst = rs->ndst;
+            p.rs_slot = rs->slot;
+            p.rs_piece = rs->piece;
+            p.rs_slot_elems = rs->slot_elems;
+            p.out = rs->dst[0];
+            p.ldo = p.npad;
+            p.part_stride = 0;
+        } else if (P.split > 1) {
             p.out = static_cast<float*>(ws);
             p.ldo = p.npad;
             p.part_stride = m * static_cast<int64_t>(p.npad);
@@ -368,7 +392,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
                                        h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream, P.cl);
         }
         if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
-        if (P.split > 1) {
+        if (P.split > 1 && !rs) {
             LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, stream);
             e = sk::launch_splitk_reduce(static_cast<const float*>(ws), p.part_stride, P.split,
                                          p.n1, p.r_valid, p.npad, B + c0, ldb, stream);
@@ -608,7 +632,7 @@ sk_status_t sketch_workspace_size(sk_sketch_t h, int64_t n1, size_t* bytes) {
 
 static sk_status_t validate_apply(sk_sketch_t h, const float* A, int64_t m, int64_t k, int64_t lda,
                                   int64_t k0, const float* B, int64_t ldb, void* ws,
-                                  size_t ws_bytes) {
+                                  size_t ws_bytes, bool check_ws = true) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
     if (sk_status_t st = check_mode(h)) return st;
     if (m < 0 || k < 1) return fail(SK_ERR_INVALID_VALUE, "need m >= 0 and k >= 1");
@@ -619,6 +643,7 @@ static sk_status_t validate_apply(sk_sketch_t h, const float* A, int64_t m, int6
     if (lda < k) return fail(SK_ERR_SHAPE_MISMATCH, "lda < number of columns of A");
     if (ldb < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "ldb < r");
     if (!aligned16(A) || (lda & 3)) return fail(SK_ERR_ALIGNMENT, "A must be 16-byte aligned with lda % 4 == 0");
+    if (!check_ws) return SK_SUCCESS;
     size_t need = 0;
     sketch_workspace_size(h, m, &need);
     if (ws_bytes < need || (need > 0 && !ws))
@@ -641,6 +666,53 @@ sk_status_t sketch_apply_block(sk_sketch_t h, const float* A_blk, int64_t m, int
     if (sk_status_t st = validate_apply(h, A_blk, m, k, lda, k0, B_part, ldb, ws, ws_bytes)) return st;
     return apply_impl(h, A_blk, m, k, lda, k0, B_part, ldb, ws, ws_bytes,
                       static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t sketch_rs_split(sk_sketch_t h, int64_t m, int64_t k, int32_t* split) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (!split || m < 1 || k < 1) return fail(SK_ERR_INVALID_VALUE, "bad reduce-scatter split query");
+    *split = plan_sketch(h, m, k, 127, ~size_t(0)).split;
+    return SK_SUCCESS;
+}
+
+sk_status_t sketch_apply_block_rs(sk_sketch_t h, const float* A_blk, int64_t m, int64_t k, int64_t lda,
+                                  int64_t k0, float* const* dst, int32_t ndst, int64_t piece_rows,
+                                  int32_t slot, int64_t slot_elems, int32_t split, void* stream) {
+    if (sk_status_t st = validate_apply(h, A_blk, m, k, lda, k0, A_blk, h ? h->r : 0, nullptr, 0, false))
+        return st;
+    if (h->r > 256) return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter supports r <= 256 (one column pass)");
+    if (!dst || ndst < 1 || ndst > 8) return fail(SK_ERR_INVALID_VALUE, "need 1 <= ndst <= 8 destinations");
+    if (piece_rows < 1 || (m + piece_rows - 1) / piece_rows > ndst)
+        return fail(SK_ERR_INVALID_VALUE, "row pieces exceed the destinations");
+    if (slot < 0 || split < 1) return fail(SK_ERR_INVALID_VALUE, "need slot >= 0 and split >= 1");
+    const int64_t npad = round_up(h->r, 16);
+    if ((slot_elems & 3) || slot_elems < piece_rows * npad)
+        return fail(SK_ERR_SHAPE_MISMATCH, "slot_elems must be a multiple of 4 and >= piece_rows * round_up(r, 16)");
+    RsTarget rs{};
+    for (int j = 0; j < ndst; ++j) {
+        if (!dst[j] || !aligned16(dst[j])) return fail(SK_ERR_ALIGNMENT, "destinations must be 16-byte aligned");
+        rs.dst[j] = dst[j];
+    }
+    rs.ndst = ndst;
+    rs.slot = slot;
+    rs.piece = piece_rows;
+    rs.slot_elems = slot_elems;
+    rs.split = split;
+    return apply_impl(h, A_blk, m, k, lda, k0, nullptr, 0, nullptr, 0, static_cast<cudaStream_t>(stream), &rs);
+}
+
+sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslots, int64_t slot_elems,
+                                int64_t rows, float* B, int64_t ldb, void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    const int64_t npad = round_up(h->r, 16);
+    if (rows < 0 || nslots < 1 || !slots || (rows > 0 && !B)) return fail(SK_ERR_INVALID_VALUE, "bad slot reduce");
+    if (ldb < h->r || slot_elems < rows * npad) return fail(SK_ERR_SHAPE_MISMATCH, "slot / B extents");
+    if (rows == 0) return SK_SUCCESS;
+    LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, static_cast<cudaStream_t>(stream));
+    cudaError_t e = sk::launch_splitk_reduce(slots, slot_elems, nslots, static_cast<int32_t>(rows),
+                                             static_cast<int32_t>(h->r), static_cast<int32_t>(npad), B, ldb,
+                                             static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "slot reduce launch");
 }
 
 sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb,

@@ -35,6 +35,14 @@ struct SketchGemmParams {
     uint32_t ablate;      // 0 in production; bit 0: skip Omega generation, bit 1: skip A loads
     uint64_t* trace;      // diagnostics (SK_TRACE builds): globaltimer stamps [cta][event][stage]
     int32_t trace_stages;
+    // fused reduce-scatter (f1; rs_ndst > 0): output row i goes to
+    //   rs_dst[i / rs_piece] + (rs_slot * split + s) * rs_slot_elems + (i % rs_piece) * ldo + col
+    // (peer receive buffers mapped over NVLink) instead of out
+    float* rs_dst[8];
+    int32_t rs_ndst;
+    int32_t rs_slot;
+    int64_t rs_piece;
+    int64_t rs_slot_elems;
 };
 
 struct CoreGemmParams {

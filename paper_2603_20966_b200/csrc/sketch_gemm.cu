@@ -458,6 +458,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     const int row = mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128 +
                                     q * 32 + static_cast<int>(lane);
                     float* orow = out + static_cast<int64_t>(row) * p.ldo;
+                    if (p.rs_ndst > 0 && row < p.n1) {
+                        // fused reduce-scatter: the row's partial goes straight to its owner's slot
+                        // (NVLink store into the peer's receive buffer), no local B / split partial
+                        const int64_t piece = row / p.rs_piece;
+                        orow = p.rs_dst[piece] + (static_cast<int64_t>(p.rs_slot) * p.split + s) * p.rs_slot_elems +
+                               (row - piece * p.rs_piece) * p.ldo;
+                    }
 #pragma unroll 1
                     for (int cc = 0; cc < p.npad; cc += 32) {
                         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +

@@ -30,6 +30,8 @@ Omega rows start on a Philox row-group boundary) except the last.
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 
@@ -91,7 +93,8 @@ class DistSketch:
     """
 
     def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
-                 mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128):
+                 mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128,
+                 fused_rs: bool = False):
         import torch.distributed as tdist
         self.tdist = tdist
         self.group = group
@@ -117,6 +120,10 @@ class DistSketch:
         elif layout.p2 > 1:
             self.row_group = group
         self.comm_bytes = 0
+        # f1: reduce-scatter of partial B fused into the GEMM epilogue (NVLink stores into the owners'
+        # symmetric-memory receive buffers) instead of an NCCL reduce_scatter after the GEMM
+        self.fused_rs = bool(fused_rs) and layout.p2 > 1
+        self._rs = None
 
     # ------------------------------------------------------------------ partition
     def a_block_range(self) -> tuple:
@@ -144,6 +151,8 @@ class DistSketch:
             return self.local.apply_block(A_blk, c0), (r0, r1)
         rows = r1 - r0
         per = -(-rows // p2)
+        if self.fused_rs:
+            return self._apply_fused_rs(A_blk, rows, per, c0)
         Bbar = torch.zeros((per * p2, self.r), dtype=torch.float32, device=A_blk.device)
         self.local.apply_block(A_blk, c0, out=Bbar[:rows])
         piece = torch.empty((per, self.r), dtype=torch.float32, device=A_blk.device)
@@ -151,6 +160,45 @@ class DistSketch:
         self.comm_bytes += Bbar.numel() * 4 * (p2 - 1) // p2
         a, b = self.b_piece_rows()
         return piece[: b - a], (a, b)
+
+    def _apply_fused_rs(self, A_blk, rows, per, c0):
+        """Alg. 1 line 415 with the reduce-scatter fused into the GEMM epilogue: every
+        rank's kernel stores its partial rows of piece j straight into rank (i, j)'s receive slot over
+        NVLink; after a device-side barrier each owner sums its p2 * split slots in a fixed order."""
+        import torch
+        p2 = self.layout.p2
+        npad = -(-self.r // 16) * 16
+        k = A_blk.shape[1]
+        if self._rs is None or self._rs["key"] != (rows, per, k):
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = self.row_group if self.row_group is not None else self.tdist.group.WORLD
+            # split-K partials would each cross NVLink (S x the reduce-scatter bytes): default to no
+            # split; RS_SPLIT=auto takes the local plan's choice (max over the row group)
+            if os.environ.get("SK_RS_SPLIT", "1") == "auto":
+                split = torch.tensor([self.local.rs_split(rows, k)], dtype=torch.int32, device=A_blk.device)
+                self.tdist.all_reduce(split, op=self.tdist.ReduceOp.MAX, group=grp)  # same slot layout everywhere
+                split = int(split.item())
+            else:
+                split = max(1, int(os.environ.get("SK_RS_SPLIT", "1")))
+            try:
+                symm_mem.enable_symm_mem_for_group(grp.group_name)
+            except Exception:  # pragma: no cover - newer torch enables it implicitly
+                pass
+            buf = symm_mem.empty((p2 * split * per * npad,), dtype=torch.float32, device=A_blk.device)
+            hdl = symm_mem.rendezvous(buf, grp.group_name)
+            ptrs = [int(hdl.buffer_ptrs[j]) for j in range(p2)]
+            self._rs = {"key": (rows, per, k), "buf": buf, "hdl": hdl, "ptrs": ptrs, "split": split, "npad": npad}
+        rs = self._rs
+        hdl, split = rs["hdl"], rs["split"]
+        hdl.barrier(channel=0)  # the owners have consumed the previous step's slots
+        self.local.apply_block_rs(A_blk, c0, rs["ptrs"], per, self.j, per * npad, split)
+        hdl.barrier(channel=0)  # every rank's stores have landed
+        a, b = self.b_piece_rows()
+        piece = self.local.reduce_slots(rs["buf"], p2 * split, per * npad, b - a)
+        # bytes this rank stored into other ranks' slots (split partials, rows padded to npad)
+        mine = [min(rows, (jj + 1) * per) - min(rows, jj * per) for jj in range(p2)]
+        self.comm_bytes += 4 * split * npad * (rows - mine[self.j])
+        return piece, (a, b)
 
     # ------------------------------------------------------------------ Alg. 2 (Redist)
     def nystrom_core_redist(self, A_blk):
