@@ -313,6 +313,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each step as one CUDA graph (auto: on for 1 GPU when A < 1 GB, i.e. the "
+                         "launch-latency-bound c1); per-phase times then come from a profiled eager pass")
     ap.add_argument("--fused-rs", action="store_true",
                     help="f1: column / 2D layouts reduce-scatter partial B from the GEMM epilogue over NVLink "
                          "(symmetric memory) instead of NCCL reduce_scatter")
@@ -394,11 +397,43 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    clocks = sampler.stop()
     launches = sk.launch_count() - launches0
     phases = local.profile_read()
     local.set_profiling(False)
     t_ms = e0.elapsed_time(e1)
+    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and 4.0 * n1 * n2 < 1e9)
+    graph_info = None
+    eager_ms_step = t_ms / args.steps
+    if use_graph and world == 1:
+        # the step captured once as a CUDA graph (library launches on the capture stream) and replayed:
+        # the eager pass above supplied the per-phase kernel times
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            for _ in range(2):
+                out = step()
+        stream.wait_stream(gs)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        lc0 = sk.launch_count()
+        with torch.cuda.graph(g, stream=gs):
+            out = step()
+        launches_per_step = sk.launch_count() - lc0
+        for _ in range(args.warmup):
+            g.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        h0 = time.perf_counter()
+        for _ in range(args.steps):
+            g.replay()
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_ms = e0.elapsed_time(e1)
+        launches = launches_per_step * args.steps
+        graph_info = {"replayed": True, "launches_per_step": launches_per_step,
+                      "eager_ms_per_step": eager_ms_step}
+    clocks = sampler.stop()
     comm_bytes = ds.comm_bytes / args.steps
     tmax = torch.tensor([t_ms], dtype=torch.float64, device=dev if world > 1 else "cpu")
     if world > 1:
@@ -458,6 +493,7 @@ def main():
         "roofline": roof,
         "gpu_launches": launches,
         "host_submit_ms_per_step": host_ms,
+        "cuda_graph": graph_info,
         "clocks": clocks,
         "comm": {"variant": args.variant if (W["nystrom"] and world > 1) else None,
                  "fused_reduce_scatter": bool(ds.fused_rs),
