@@ -49,6 +49,22 @@ SEED_A = {"c1": 1, "c2": 2, "c3": 3, "c4": 4}
 NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200 dense tensor peaks (B200_PROFILING.md nominal table)
 
 
+def auto_layout(wl_name, world):
+    """The processor grid BASELINE.json's configs name: c2 "2/4/8 with 2D grid" (most square p1 x p2,
+    p1 >= p2), c3 row-block (zero communication), c4 column-block (NCCL reduce-scatter of B)."""
+    if world == 1:
+        return "row"
+    if wl_name == "c4":
+        return "col"
+    if wl_name == "c2":
+        p2 = 1
+        for d in range(1, int(world ** 0.5) + 1):
+            if world % d == 0:
+                p2 = d
+        return f"{world // p2}x{p2}"
+    return "row"
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -305,7 +321,9 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="bf16", choices=["tf32", "tf32x3", "bf16"])
     ap.add_argument("--omega", default="accurate", choices=["accurate", "fast"])
-    ap.add_argument("--layout", default="row", help="row | col | AxB (p1 x p2)")
+    ap.add_argument("--layout", default="auto",
+                    help="row | col | AxB (p1 x p2) | auto = the layout BASELINE.json names for the workload "
+                         "(c2: 2D grid, c3: row-block, c4: column-block)")
     ap.add_argument("--split-k", type=int, default=0)
     ap.add_argument("--variant", default="noredist", choices=["noredist", "redist"],
                     help="Alg. 2 variant for N > 1 row-block Nystrom (PAPER.md:698)")
@@ -348,7 +366,7 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
         tdist.init_process_group("gloo", rank=0, world_size=1)
-    layout = Layout.parse(args.layout, world)
+    layout = Layout.parse(auto_layout(args.workload, world) if args.layout == "auto" else args.layout, world)
     n1, n2, r = W["n1"], W["n2"], W["r"]
     peaks = load_peaks()
 
