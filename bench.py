@@ -42,10 +42,13 @@ WORKLOADS = {
                n1=4_000_000, n2=2048, r=128, dist="rademacher", nystrom=False, a="uniform"),
     "c4": dict(desc="c4: short-wide A 2,048x4,000,000 fp32 U[-1/2,1/2), r=512 Gaussian",
                n1=2048, n2=4_000_000, r=512, dist="gaussian", nystrom=False, a="uniform"),
+    "c5": dict(desc="c5: large symmetric PSD A n=200,000 (RBF kernel of X~U[0,1)^{200000x64}; 160 GB, "
+                    "for 8 GPUs), Nystrom r=1,024, 2D grid, AllReduce of C",
+               n1=200_000, n2=200_000, r=1024, dist="gaussian", nystrom=True, a="rbf", d=64),
 }
 
 SEED_OMEGA = 42
-SEED_A = {"c1": 1, "c2": 2, "c3": 3, "c4": 4}
+SEED_A = {"c1": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}
 NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200 dense tensor peaks (B200_PROFILING.md nominal table)
 
 
@@ -56,7 +59,7 @@ def auto_layout(wl_name, world):
         return "row"
     if wl_name == "c4":
         return "col"
-    if wl_name == "c2":
+    if wl_name in ("c2", "c5"):
         p2 = 1
         for d in range(1, int(world ** 0.5) + 1):
             if world % d == 0:

@@ -200,6 +200,22 @@ def test_nystrom_core_parity(n, r, mode):
     assert _relF(C.cpu().numpy(), Cown) <= TOL[mode]
 
 
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+def test_c5_shape_four_column_passes_clusters(mode):
+    """c5's r = 1024 at a shape that takes clusters of 4 CTA pairs: four 256-column passes of the
+    sketch and the fp32 SIMT core (r > 256), against the oracle on sampled rows and on C."""
+    sk = _sk()
+    n, r = 4100, 1024
+    A = synth.symmetric_uniform(8, n)
+    s = sk.Sketch(SEED, "gaussian", n, r, mode=mode)
+    B, C = s.nystrom_core(_dev(A))
+    rows = np.linspace(0, n - 1, 40).astype(int)
+    Bref_rows = oracle.sketch(SEED, "gaussian", A[rows], r)
+    assert _relF(B.cpu().numpy()[rows], Bref_rows) <= TOL[mode]
+    Cown = oracle.core(SEED, "gaussian", B.cpu().numpy().astype(np.float64))
+    assert _relF(C.cpu().numpy(), Cown) <= TOL[mode]
+
+
 def test_nystrom_core_integer_exact():
     sk = _sk()
     A, X = synth.lowrank_psd(3, 1024, 8, -2, 2)
