@@ -286,14 +286,17 @@ CorePlan plan_core_simt(const sk_sketch_s* h, int64_t m) {
 // tcgen05 core for r <= 256 (one CTA per 128-aligned chunk of about m / #SMs rows); SIMT otherwise.
 CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0) {
     // tf32x3 keeps C fp32-accurate with the fp32-FMA core (a 3xTF32 core is future work)
-    if (h->r > 256 || h->core_simt || h->mode == sk::kTF32x3) return plan_core_simt(h, m);
+    if (h->core_simt || h->mode == sk::kTF32x3) return plan_core_simt(h, m);
     CorePlan C{};
     C.tc = true;
-    C.npad = static_cast<int>(round_up(h->r, 16));
+    // r or nb > 256: 256 x 256 blocks of C, one CTA per (row chunk, block); the chunk count shrinks
+    // so that the grid stays about one wave
+    C.npad = static_cast<int>(std::min<int64_t>(256, round_up(h->r, 16)));
     C.nacc = h->r > 128 ? 2 : 1;
     C.base = i0 & ~static_cast<int64_t>(127);
     const int64_t span = std::max<int64_t>(1, i0 + m - C.base);
-    const int64_t want = sk::num_sms();
+    const int64_t blocks = ((h->r + 255) / 256) * ((h->r + 255) / 256);
+    const int64_t want = std::max<int64_t>(1, sk::num_sms() / blocks);
     C.step = round_up((span + want - 1) / want, 128);
     C.chunks = static_cast<int>((span + C.step - 1) / C.step);
     return C;
@@ -420,7 +423,7 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         q.m = static_cast<int32_t>(m);
         q.r = static_cast<int32_t>(h->r);
         q.nb = static_cast<int32_t>(nb);
-        q.npad = static_cast<int32_t>(round_up(nb, 16));
+        q.npad = static_cast<int32_t>(std::min<int64_t>(256, round_up(nb, 16)));
         q.nchunks = CP.chunks;
         q.key0 = static_cast<uint32_t>(h->seed);
         q.key1 = static_cast<uint32_t>(h->seed >> 32);

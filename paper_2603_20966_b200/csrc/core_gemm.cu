@@ -110,7 +110,8 @@ cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaS
 }  // namespace sk
 
 // =============================================================================================
-// tcgen05 core GEMM (r <= 256): one CTA per K-chunk of B rows computes the whole r x r partial.
+// tcgen05 core GEMM: CTA (chunk, ablk, bblk) computes the 256 x 256 block (ablk, bblk) of the r x nb
+// partial of its K-chunk of B rows (one block when r, nb <= 256).
 //   D[a, b] += OmegaT[a, i] * B[i, b]:  M = Omega columns a (NACC blocks of 128), N = npad (b),
 //   K = rows i in 32-row steps, kind::tf32, fp32 accumulators in TMEM.
 //   * Omega^T tile (A operand, K-major SW128) is regenerated by 16 producer warps with the sketch
@@ -172,6 +173,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int chunk = blockIdx.x;
+    const int a_off = static_cast<int>(blockIdx.y) * 256;  // first Omega column (row of C) of this block
+    const int b_off = static_cast<int>(blockIdx.z) * 256;  // first column of B / C of this block
     const int64_t g0 = p.base + static_cast<int64_t>(chunk) * p.step;  // aligned global row
     const int64_t gend = min(p.i0 + static_cast<int64_t>(p.m), g0 + p.step);
     const int ksteps = static_cast<int>((gend - g0 + 31) / 32);
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
                 mbar_arrive_expect_tx(&full_raw[st], L.raw_stage);
                 const int32_t row = static_cast<int32_t>(g0 - p.i0) + 32 * t;  // may be < 0: zero fill
                 for (int gcol = 0; gcol < ngrp; ++gcol)
-                    tma_load_2d(sRaw + st * L.raw_stage + gcol * 4096, &tmB, &full_raw[st], gcol * 32, row, pol);
+                    tma_load_2d(sRaw + st * L.raw_stage + gcol * 4096, &tmB, &full_raw[st], b_off + gcol * 32, row, pol);
                 if (++st == kCoreRawStages) { st = 0; ph ^= 1; }
             }
         }
@@ -238,9 +241,9 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             mbar_wait(&empty_op[so], po ^ 1);
             uint8_t* o_tile = sO + so * L.o_stage;
             if constexpr (DIST == kRademacher)
-                produce_omega_tile_r<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, 0, p.key0, p.key1, tt);
+                produce_omega_tile_r<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, a_off, p.key0, p.key1, tt);
             else
-                produce_omega_tile_g<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, 0, p.key0, p.key1,
+                produce_omega_tile_g<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, a_off, p.key0, p.key1,
                                                        n_start, j_start, tq, tr);
             // transpose the raw B tile (32 rows i x npad cols b, 128-B rows per 32-col group) into
             // the K-major SW128 tile: row b, chunk j4 = rows 4 j4 .. 4 j4 + 3
@@ -277,9 +280,9 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             int ebuf = 0;
 #pragma unroll 1
             for (int a = 0; a < NACC; ++a) {
-                const int row = a * 128 + q * 32 + static_cast<int>(lane);  // Omega column a
-                float* orow = out + static_cast<int64_t>(row) * p.ldp;
-                if (p.tma_store && a * 128 + q * 32 >= p.r) continue;  // padding rows of the last block
+                const int row = a_off + a * 128 + q * 32 + static_cast<int>(lane);  // Omega column a
+                float* orow = out + static_cast<int64_t>(row) * p.ldp + b_off;
+                if (p.tma_store && a_off + a * 128 + q * 32 >= p.r) continue;  // padding rows of the last block
 #pragma unroll 1
                 for (int cc = 0; cc < p.npad; cc += 32) {
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -295,11 +298,11 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
                     }
                     tmem_ld_wait();
                     if (p.tma_store) {
-                        epi_store_tile(&tmOut, epi, ebuf, v, cc, chunk * p.r + a * 128 + q * 32);
+                        epi_store_tile(&tmOut, epi, ebuf, v, b_off + cc, chunk * p.r + a_off + a * 128 + q * 32);
                     } else if (row < p.r) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
-                            if (cc + i < p.nb) orow[cc + i] = __uint_as_float(v[i]);
+                            if (b_off + cc + i < p.nb) orow[cc + i] = __uint_as_float(v[i]);
                     }
                 }
             }
@@ -327,7 +330,8 @@ static cudaError_t launch_core_tc_one(const CUtensorMap& tmB, const CUtensorMap&
         if (e != cudaSuccess) return e;
         smem_set = smem;
     }
-    kern<<<p.nchunks, kCoreThreads, smem, s>>>(tmB, tmOut, p);
+    const dim3 grid(p.nchunks, (p.r + 255) / 256, (p.nb + 255) / 256);
+    kern<<<grid, kCoreThreads, smem, s>>>(tmB, tmOut, p);
     return cudaGetLastError();
 }
 

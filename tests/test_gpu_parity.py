@@ -203,7 +203,7 @@ def test_nystrom_core_parity(n, r, mode):
 @pytest.mark.parametrize("mode", ["tf32", "bf16"])
 def test_c5_shape_four_column_passes_clusters(mode):
     """c5's r = 1024 at a shape that takes clusters of 4 CTA pairs: four 256-column passes of the
-    sketch and the fp32 SIMT core (r > 256), against the oracle on sampled rows and on C."""
+    sketch and the tcgen05 core in 16 blocks of 256 x 256, against the oracle on sampled rows and on C."""
     sk = _sk()
     n, r = 4100, 1024
     A = synth.symmetric_uniform(8, n)
@@ -229,7 +229,7 @@ def test_nystrom_core_integer_exact():
 
 @pytest.mark.parametrize("core", ["auto", "simt"])
 @pytest.mark.parametrize("i0", [0, 5, 130, 4000])
-@pytest.mark.parametrize("r", [48, 256, 16])
+@pytest.mark.parametrize("r", [48, 256, 16, 300, 640])
 def test_core_block(i0, r, core):
     sk = _sk()
     Bm = synth.uniform(8, 5000, r).astype(np.float32)
@@ -384,11 +384,11 @@ def test_nystrom_error_decreases_with_rank_gpu():
 
 
 @pytest.mark.parametrize("core", ["auto", "simt"])
-@pytest.mark.parametrize("nb", [1, 7, 64, 100])
-def test_core_block_cols(nb, core):
-    """Column-block core for the Redist variant: C[:, cols] = Omega^T B[:, cols] (all r rows of C)."""
+@pytest.mark.parametrize("nb,r", [(1, 128), (7, 128), (64, 128), (100, 128), (300, 512), (520, 520)])
+def test_core_block_cols(nb, r, core):
+    """Column-block core for the Redist variant: C[:, cols] = Omega^T B[:, cols] (all r rows of C);
+    r or nb > 256 take several 256 x 256 blocks of C."""
     sk = _sk()
-    r = 128
     Bm = synth.int_matrix(17, 3000, nb, -8, 8)
     s = sk.Sketch(SEED, "rademacher", 5000, r, mode="tf32", core=core)
     Cc = s.core_block_cols(_dev(Bm), 77).cpu().numpy()
