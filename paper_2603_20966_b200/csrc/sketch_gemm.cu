@@ -158,8 +158,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // A_lo -- and the peer's completion is relayed to the leader: leader count 2)
         for (int s = 0; s < p.a_stages; ++s) {
             mbar_init(&full_a[s], 1);
-            // bf16 / tf32x3: the converter warps' arrivals; the pair leader also counts the peer's relay
-            mbar_init(&conv[s], kCvtWarps + ((CG == 2 && leader) ? 1 : 0));
+            // bf16 / tf32x3: the converter warps' arrivals; the pair leader also counts the peer's converter
+            // warps, which arrive on it directly (relaxed, remote)
+            mbar_init(&conv[s], kCvtWarps * ((CG == 2 && leader) ? 2 : 1));  // + the peer's warps (remote)
             mbar_init(&empty_a[s], 1);
         }
         for (int s = 0; s < p.o_stages; ++s) {
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // warp 1) pushes this CTA's Omega half into the partner pair's CTA.
         const bool is_copier = (CL > 1) && ((leader && warp == 3) || (!leader && warp == 1));
         const bool is_orelay = (CG == 2) && (CL > 1) && !leader && warp == 2;
-        const bool is_arelay = ARELAY && !leader && warp == 3;
+        const bool is_arelay = false;  // (the peer's converter warps arrive on the leader directly)
         if ((is_copier || is_orelay || is_arelay) && elect_one()) {
             uint64_t* bars_r = is_orelay ? full_o : conv;
             const uint32_t nst = static_cast<uint32_t>(is_arelay ? p.a_stages : p.o_stages);
@@ -531,7 +532,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&conv[sa]);
+                if (lane == 0) {
+                    if (CG == 2 && !leader) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&conv[sa]), lead_rank));
+                    else mbar_arrive(&conv[sa]);
+                }
                 if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
             }
         }
@@ -599,7 +603,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&empty_y[ys]);
-                    mbar_arrive(&conv[sa]);
+                    if (CG == 2 && !leader) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&conv[sa]), lead_rank));
+                    else mbar_arrive(&conv[sa]);
                 }
                 if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                 if (++ys == static_cast<uint32_t>(p.y_stages)) ys = 0;
