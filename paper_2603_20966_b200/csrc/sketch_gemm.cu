@@ -152,10 +152,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     while (tmem_cols < static_cast<uint32_t>(NACC * p.npad)) tmem_cols <<= 1;
 
     if (warp == 0 && lane == 0) {
-        // full_a: one expect_tx arrival; with CG = 2 the leader's barrier counts the bytes of BOTH
-        // CTAs' TMA loads (the peer's loads complete_tx on it directly)
-        // (tf32x3 pairs: each CTA's A lands on its own barrier -- its producers read it to form
-        // A_lo -- and the peer's completion is relayed to the leader: leader count 2)
+        // full_a: one expect_tx arrival; with CG = 2 (tf32) the leader's barrier counts the bytes of
+        // BOTH CTAs' TMA loads (the peer's loads complete_tx on it directly).  bf16 / tf32x3: each
+        // CTA's A lands on its own barrier (its converter warps read it) and the MMA waits on conv.
         for (int s = 0; s < p.a_stages; ++s) {
             mbar_init(&full_a[s], 1);
             // bf16 / tf32x3: the converter warps' arrivals; the pair leader also counts the peer's converter
