@@ -139,6 +139,8 @@ struct SketchPlan {
     int cl;            // 2: clusters of two CTA pairs sharing every generated Omega slice
     int nacc;
     int a_stages, o_stages, y_stages;
+    int64_t sk_len;    // > 0: stream-K range length per worker (split = max pieces per m-block)
+    int rows_per_unit;
     int split;
     int kiters;
     int num_mblk;
@@ -201,7 +203,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // shared bytes (6.2 -> 7.1 ms with sharing); then 2 pairs, then none if the shape does not allow
     // it.  sketch_set_cta_group(h, 2 / 4 / 8) forces none / 2 pairs / 4 pairs.
     auto cl_ok = [&](int cl) {
-        return P.cg == 2 && P.nacc == 2 && n1 >= 1024 * cl && npad_max % (16 * cl) == 0 && h->dist == sk::kGaussian;
+        return P.cg == 2 && P.nacc == 2 && n1 >= 512 * cl && npad_max % (16 * cl) == 0 && h->dist == sk::kGaussian;
     };
     P.cl = 1;
     if (h->cl_override == 0 && !x3) P.cl = cl_ok(4) ? 4 : cl_ok(2) ? 2 : 1;
@@ -229,9 +231,10 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
         best_s = std::min(h->split_override, std::max(1, P.kiters));
     } else if (min_split > 64) {
         best_s = min_split;
-    } else {
-        double best = 1e300;
-        const double unit_ovh = 2.0;  // epilogue + pipeline fill, in K-iteration units
+    }
+    double best = 1e300;
+    const double unit_ovh = 2.0;  // epilogue + pipeline fill, in K-iteration units
+    if (force_split == 0 && h->split_override == 0 && min_split <= 64) {
         for (int s = min_split; s <= std::max(min_split, std::min(64, std::max(1, P.kiters / 4))); ++s) {
             const int64_t units = static_cast<int64_t>(P.num_mblk) * s;
             const int64_t waves = (units + nsm - 1) / nsm;
@@ -250,11 +253,30 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     P.split = (P.kiters + kper - 1) / kper;
     const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
     P.grid = static_cast<int>(std::min<int64_t>(units, nsm)) * P.cg * P.cl;
+    P.rows_per_unit = rows_per_unit;
+    P.sk_len = 0;
+    // Stream-K: every worker gets the same number of K iterations of the flattened (m-block, K)
+    // space, cut at m-block boundaries, when wave quantisation of the split-K units would leave
+    // workers idle (e.g. 13 m-blocks on 15 clusters).  Not for tf32x3 (K per accumulator is capped)
+    // or an explicit split (fused reduce-scatter slots, tests).
+    if (!x3 && force_split == 0 && h->split_override == 0 && getenv("SK_NO_STREAMK") == nullptr && best < 1e299) {
+        const int64_t total = static_cast<int64_t>(P.num_mblk) * P.kiters;
+        const int64_t L = (total + nsm - 1) / nsm;
+        const int pieces = static_cast<int>((P.kiters + L - 1) / L) + 1;
+        const double t_sk = static_cast<double>(L) + unit_ovh * (1.0 + static_cast<double>(L) / P.kiters) +
+                            static_cast<double>(pieces + 1) * n1 * npad_max * 4.0 /
+                                (static_cast<double>(nsm) * a_stage * P.cg);
+        if (t_sk < best * 0.97 && ws_cap >= static_cast<size_t>(pieces) * P.ws_per_split) {
+            P.sk_len = L;
+            P.split = pieces;
+            P.grid = static_cast<int>((total + L - 1) / L) * P.cg * P.cl;
+        }
+    }
     if ((h->ablate & 8u) && (P.grid & 1)) P.grid += 1;  // cluster-of-2 ablation needs an even grid
     if (getenv("SK_DEBUG_PLAN"))  // tuning diagnostics
-        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d a=%d y=%d o=%d split=%d kiters=%d mblk=%d grid=%d smem=%zu\n",
+        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d a=%d y=%d o=%d split=%d sk_len=%lld kiters=%d mblk=%d grid=%d smem=%zu\n",
                 static_cast<long long>(n1), static_cast<long long>(k), P.cg, P.cl, P.nacc, P.a_stages, P.y_stages,
-                P.o_stages, P.split, P.kiters, P.num_mblk, P.grid, P.smem);
+                P.o_stages, P.split, static_cast<long long>(P.sk_len), P.kiters, P.num_mblk, P.grid, P.smem);
     return P;
 }
 
@@ -364,6 +386,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.o_stages = P.o_stages;
         p.y_stages = P.y_stages;
         p.prefetch = 0;
+        p.sk_len = P.sk_len;
         if (const char* e = getenv("SK_PREFETCH")) p.prefetch = std::max(0, std::min(16, atoi(e)));  // tuning
         p.key0 = static_cast<uint32_t>(h->seed);
         p.key1 = static_cast<uint32_t>(h->seed >> 32);
@@ -379,7 +402,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
             p.out = rs->dst[0];
             p.ldo = p.npad;
             p.part_stride = 0;
-        } else if (P.split > 1) {
+        } else if (P.split > 1 || P.sk_len > 0) {
             p.out = static_cast<float*>(ws);
             p.ldo = p.npad;
             p.part_stride = m * static_cast<int64_t>(p.npad);
@@ -395,7 +418,12 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
                                        h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream, P.cl);
         }
         if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
-        if (P.split > 1 && !rs) {
+        if (P.sk_len > 0 && !rs) {
+            LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, stream);
+            e = sk::launch_streamk_reduce(static_cast<const float*>(ws), p.part_stride, p.n1, p.r_valid, p.npad,
+                                          B + c0, ldb, P.rows_per_unit, P.kiters, P.sk_len, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "streamk_reduce launch");
+        } else if (P.split > 1 && !rs) {
             LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, stream);
             e = sk::launch_splitk_reduce(static_cast<const float*>(ws), p.part_stride, P.split,
                                          p.n1, p.r_valid, p.npad, B + c0, ldb, stream);

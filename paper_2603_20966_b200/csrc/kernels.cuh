@@ -31,6 +31,9 @@ struct SketchGemmParams {
     int32_t o_stages;     // Omega smem pipeline depth
     int32_t y_stages;     // bf16: depth of the ring holding K 32..63 of each fp32 A stage
     int32_t prefetch;     // K steps of A prefetched into L2 ahead of the TMA loads (0 = off)
+    int64_t sk_len;       // > 0: stream-K -- worker w runs flattened (m-block, K-iteration) indices
+                          // [w sk_len, (w+1) sk_len), cut at m-block boundaries; partial `piece` =
+                          // w - first worker touching the m-block (split / kper unused)
     uint32_t key0, key1;  // Philox key = (seed lo, seed hi)
     uint32_t ablate;      // 0 in production; bit 0: skip Omega generation, bit 1: skip A loads
     uint64_t* trace;      // diagnostics (SK_TRACE builds): globaltimer stamps [cta][event][stage]
@@ -94,6 +97,9 @@ size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_st
                               bool olo, int ks, int nsubo, int y_stages);
 int sketch_gemm_max_smem();
 
+cudaError_t launch_streamk_reduce(const float* part, int64_t part_stride, int32_t n1, int32_t r_valid,
+                                  int32_t ldp, float* out, int64_t ldo, int32_t rows_per_unit, int32_t kiters,
+                                  int64_t sk_len, cudaStream_t s);
 cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t split,
                                  int32_t n1, int32_t r_valid, int32_t ldp, float* out,
                                  int64_t ldo, cudaStream_t s);

@@ -61,6 +61,65 @@ cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t
     return cudaGetLastError();
 }
 
+// Stream-K partials: row i belongs to m-block mb = i / rows_per_unit, whose K iterations were cut by
+// the workers' ranges into pieces 0 .. last - first (first / last = first and last worker touching
+// the m-block); out[i, c] = sum of those pieces in increasing piece (= K) order.
+__global__ void streamk_reduce_kernel_v4(const float4* __restrict__ part, int64_t part_stride4, int32_t n1,
+                                         int32_t r4, int32_t ldp4, float4* __restrict__ out, int64_t ldo4,
+                                         int32_t rows_per_unit, int32_t kiters, int64_t sk_len) {
+    const int64_t total = static_cast<int64_t>(n1) * r4;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / r4;
+        const int64_t c = idx - i * r4;
+        const int64_t mb = i / rows_per_unit;
+        const int64_t first = (mb * kiters) / sk_len, last = ((mb + 1) * kiters - 1) / sk_len;
+        const float4* p = part + i * ldp4 + c;
+        float4 acc = __ldg(p);
+        for (int64_t s = 1; s <= last - first; ++s) {
+            const float4 v = __ldg(p + s * part_stride4);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        out[i * ldo4 + c] = acc;
+    }
+}
+
+__global__ void streamk_reduce_kernel(const float* __restrict__ part, int64_t part_stride, int32_t n1,
+                                      int32_t r_valid, int32_t ldp, float* __restrict__ out, int64_t ldo,
+                                      int32_t rows_per_unit, int32_t kiters, int64_t sk_len) {
+    const int64_t total = static_cast<int64_t>(n1) * r_valid;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / r_valid;
+        const int64_t c = idx - i * r_valid;
+        const int64_t mb = i / rows_per_unit;
+        const int64_t first = (mb * kiters) / sk_len, last = ((mb + 1) * kiters - 1) / sk_len;
+        const float* p = part + i * ldp + c;
+        float acc = __ldg(p);
+        for (int64_t s = 1; s <= last - first; ++s) acc += __ldg(p + s * part_stride);
+        out[i * ldo + c] = acc;
+    }
+}
+
+cudaError_t launch_streamk_reduce(const float* part, int64_t part_stride, int32_t n1, int32_t r_valid,
+                                  int32_t ldp, float* out, int64_t ldo, int32_t rows_per_unit, int32_t kiters,
+                                  int64_t sk_len, cudaStream_t s) {
+    if (n1 <= 0 || r_valid <= 0) return cudaSuccess;
+    const int threads = 256;
+    const bool v4 = (r_valid % 4 == 0) && (ldp % 4 == 0) && (ldo % 4 == 0) && (part_stride % 4 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((reinterpret_cast<uintptr_t>(part) & 15) == 0);
+    const int64_t total = static_cast<int64_t>(n1) * (v4 ? r_valid / 4 : r_valid);
+    const int blocks = static_cast<int>(std::min<int64_t>((total + threads - 1) / threads, 148 * 16));
+    if (v4)
+        streamk_reduce_kernel_v4<<<blocks, threads, 0, s>>>(
+            reinterpret_cast<const float4*>(part), part_stride / 4, n1, r_valid / 4, ldp / 4,
+            reinterpret_cast<float4*>(out), ldo / 4, rows_per_unit, kiters, sk_len);
+    else
+        streamk_reduce_kernel<<<blocks, threads, 0, s>>>(part, part_stride, n1, r_valid, ldp, out, ldo,
+                                                         rows_per_unit, kiters, sk_len);
+    return cudaGetLastError();
+}
+
 // C[a, b] = sum_{c < chunks} part[c][a][b], r x nb, fixed order.
 __global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r, int32_t nb,
                                    float* __restrict__ C, int64_t ldc) {

@@ -52,6 +52,40 @@ __device__ __forceinline__ void trace_stamp(const SketchGemmParams& p, int ev, u
     (void)p; (void)ev; (void)i;
 #endif
 }
+// Work decomposition shared by every warp role (they must see the same segment sequence):
+// split-K units u = group, group + ngroups, ... (m-block u / split, K slice u % split), or stream-K
+// (p.sk_len > 0): the worker's contiguous range of flattened (m-block, K-iteration) indices, cut at
+// m-block boundaries, so that every worker gets the same number of K iterations.
+struct WorkIter {
+    int64_t it, end;
+    int u, group;
+    __device__ __forceinline__ WorkIter(const SketchGemmParams& p, int g) : it(0), end(0), u(g), group(g) {
+        if (p.sk_len > 0) {
+            it = static_cast<int64_t>(g) * p.sk_len;
+            end = min(it + p.sk_len, static_cast<int64_t>(p.num_mblk) * p.kiters);
+        }
+    }
+    __device__ __forceinline__ bool next(const SketchGemmParams& p, int ngroups, int& mb, int& kb, int& ke,
+                                         int& piece) {
+        if (p.sk_len > 0) {
+            if (it >= end) return false;
+            mb = static_cast<int>(it / p.kiters);
+            kb = static_cast<int>(it - static_cast<int64_t>(mb) * p.kiters);
+            ke = static_cast<int>(min(static_cast<int64_t>(p.kiters), kb + (end - it)));
+            piece = group - static_cast<int>((static_cast<int64_t>(mb) * p.kiters) / p.sk_len);
+            it += ke - kb;
+            return true;
+        }
+        if (u >= p.num_mblk * p.split) return false;
+        mb = u / p.split;
+        piece = u - mb * p.split;
+        kb = piece * p.kper;
+        ke = min(kb + p.kper, p.kiters);
+        u += ngroups;
+        return true;
+    }
+};
+
 constexpr uint32_t kATileBytes = 128 * 32 * 4;  // one 128-row x 32-fp32 TMA box
 constexpr int kMaxStages = 8;
 
@@ -187,7 +221,6 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int total_units = p.num_mblk * p.split;
     const int rows_per_unit = 128 * CG * NACC * CL;   // rows of a work unit (all pairs of a cluster)
     const int pair_row0 = static_cast<int>(pairq) * 128 * CG * NACC;  // this pair's rows inside a unit
 
@@ -197,9 +230,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             const uint64_t pol = l2_policy_evict_first();
             const uint32_t a_bytes_cta = ALO ? L.a_stage / 2 : L.a_stage;  // (tf32x3: A_lo not loaded)
             uint32_t st = 0, ph = 0, ntr = 0, yst = 0, yph = 0;
-            for (int u = group; u < total_units; u += ngroups) {
-                const int mb = u / p.split, s = u - (u / p.split) * p.split;
-                const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+            WorkIter wi(p, group);
+            int mb, kb, ke, s;
+            while (wi.next(p, ngroups, mb, kb, ke, s)) {
                 // L2 prefetch of A, p.prefetch K steps ahead of the loads: the HBM latency under load
                 // (~1.6 us) then overlaps the smem ring instead of adding to each stage's turnaround
                 auto prefetch = [&](int kp) {
@@ -266,9 +299,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         if (elect_one()) {
             const uint32_t idesc = make_idesc(BF ? kFmtBF16 : kFmtTF32, 128 * CG, static_cast<uint32_t>(p.npad), 0, 0);
             uint32_t sa = 0, pa = 0, so = 0, po = 0, local = 0, ntr = 0;
-            for (int u = group; u < total_units; u += ngroups, ++local) {
-                const int s = u - (u / p.split) * p.split;
-                const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+            WorkIter wi(p, group);
+            int mb, kb, ke, s;
+            for (; wi.next(p, ngroups, mb, kb, ke, s); ++local) {
                 mbar_wait(tmem_empty, (local & 1) ^ 1);
                 tc_fence_after();
                 for (int kit = kb; kit < ke; ++kit, ++ntr) {
@@ -344,9 +377,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             const uint32_t half_off = pairq * half_bytes;
             const uint32_t tx = half_bytes * (OLO ? 2u : 1u) * NSUBO * (CL - 1);
             uint32_t st = 0, ph = 0, ntr = 0;
-            for (int u = group; u < total_units; u += ngroups) {
-                const int s = u - (u / p.split) * p.split;
-                const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+            WorkIter wi(p, group);
+            int mb, kb, ke, s;
+            while (wi.next(p, ngroups, mb, kb, ke, s)) {
                 for (int kit = kb; kit < ke; ++kit, ++ntr) {
                     if (is_copier) {
                         mbar_wait(&gen_done[st], ph);
@@ -396,9 +429,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
         uint32_t so = 0, po = 0, sa = 0, pa = 0, local = 0, ntr = 0;
         const uint32_t lo_off = L.olo_off - L.ohi_off;
-        for (int u = group; u < total_units; u += ngroups, ++local) {
-            const int mb = u / p.split, s = u - (u / p.split) * p.split;
-            const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+        WorkIter wi(p, group);
+        int mb, kb, ke, s;
+        for (; wi.next(p, ngroups, mb, kb, ke, s); ++local) {
             for (int kit = kb; kit < ke; ++kit, ++ntr) {
                 if (p.ablate & 32u) mbar_wait(&empty_o[so], po ^ 1);
                 else mbar_wait_sleep(&empty_o[so], po ^ 1);
@@ -451,7 +484,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 const int q = t >> 5;
                 mbar_wait(tmem_full, local & 1);
                 tc_fence_after();
-                float* out = p.out + (p.split > 1 ? static_cast<int64_t>(s) * p.part_stride : 0);
+                float* out = p.out + ((p.split > 1 || p.sk_len > 0) ? static_cast<int64_t>(s) * p.part_stride : 0);
                 const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
                 for (int a = 0; a < NACC; ++a) {
@@ -510,9 +543,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         const int cw = static_cast<int>(warp) - (kCtlWarps + kRngW);
         const int ct = cw * 32 + static_cast<int>(lane);
         uint32_t sa = 0, pa = 0;
-        for (int u = group; u < total_units; u += ngroups) {
-            const int s = u - (u / p.split) * p.split;
-            const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+        WorkIter wi(p, group);
+        int mb, kb, ke, s;
+        while (wi.next(p, ngroups, mb, kb, ke, s)) {
             for (int kit = kb; kit < ke; ++kit) {
                 if (cw == 0) mbar_wait(&full_a[sa], pa);
                 asm volatile("bar.sync 2, %0;" ::"n"(kCvtWarps * 32) : "memory");
@@ -555,9 +588,9 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         constexpr int kRowsPerPass = kCvtWarps * 4;        // 4 rows per warp per item
         constexpr int kUnroll = 4;
         uint32_t sa = 0, pa = 0, ys = 0, ntr = 0;
-        for (int u = group; u < total_units; u += ngroups) {
-            const int s = u - (u / p.split) * p.split;
-            const int kb = s * p.kper, ke = min(kb + p.kper, p.kiters);
+        WorkIter wi(p, group);
+        int mb, kb, ke, s;
+        while (wi.next(p, ngroups, mb, kb, ke, s)) {
             for (int kit = kb; kit < ke; ++kit, ++ntr) {
                 // converter warp 0 polls, a named barrier releases the other converter warps
                 if (cw == 0) mbar_wait(&full_a[sa], pa);
