@@ -396,3 +396,30 @@ def test_core_block_cols(nb, r, core):
     Bpad[:, :nb] = Bm
     ref = oracle.core(SEED, "rademacher", Bpad, i0=77)[:, :nb]
     assert Cc.shape == (r, nb) and np.array_equal(Cc.astype(np.float64), ref)
+
+
+# ----------------------------------------------------------------------------- stream-K decomposition
+@pytest.mark.parametrize("dist,mode", [("gaussian", "bf16"), ("gaussian", "tf32"), ("rademacher", "tf32")])
+def test_streamk_matches_oracle(dist, mode, capfd, monkeypatch):
+    """A shape whose split-K waves would idle workers runs stream-K (equal K ranges per cluster / pair,
+    m-blocks cut into pieces summed in K order): B equals the oracle (exactly in the integer regime)
+    and reruns are bit-identical."""
+    sk = _sk()
+    monkeypatch.setenv("SK_DEBUG_PLAN", "1")
+    n1, n2, r = 6250, 16384, (256 if dist == "gaussian" else 128)
+    A = synth.int_matrix(23, n1, n2, -4, 4) if dist == "rademacher" else synth.uniform(23, n1, n2)
+    s = sk.Sketch(SEED, dist, n2, r, mode=mode)
+    B1 = s.apply(_dev(A))
+    B2 = s.apply(_dev(A))
+    torch.cuda.synchronize()
+    err = capfd.readouterr().err
+    plans = [l for l in err.splitlines() if l.startswith("[sketch plan]") and f"n1={n1}" in l]
+    assert plans and all("sk_len=0" not in l for l in plans), plans[:2]
+    assert torch.equal(B1, B2)
+    rows = np.linspace(0, n1 - 1, 32).astype(int)
+    ref = oracle.sketch(SEED, dist, A[rows].astype(np.float64), r)
+    got = B1.cpu().numpy()[rows]
+    if dist == "rademacher":
+        assert np.array_equal(got.astype(np.float64), ref)
+    else:
+        assert _relF(got, ref) <= TOL[mode]
