@@ -362,16 +362,15 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         }
     } else if (warp == 2 || warp == 3 || (warp == 1 && !leader)) {
         // ------------------------------------------------------------------ relays / copier
-        // Peer CTA: warp 2 forwards its full_o and warp 3 its conv (bf16) / full_a (tf32x3) to the pair leader
-        // with a RELAXED cluster-scope arrive (a release.cluster arrive drains in-flight TMA
-        // traffic; the relay writes nothing itself).  CL = 2: the copier (leader: warp 3, peer:
-        // warp 1) pushes this CTA's Omega half into the partner pair's CTA.
+        // CL > 1: the peer CTA's warp 2 forwards its full_o (own share written + partners' bytes
+        // landed) to the pair leader with a RELAXED cluster-scope arrive (a release.cluster arrive
+        // drains in-flight TMA traffic; the relay writes nothing itself), and the copier (leader:
+        // warp 3, peer: warp 1) bulk-copies this CTA's Omega share into the partner pairs' CTAs.
         const bool is_copier = (CL > 1) && ((leader && warp == 3) || (!leader && warp == 1));
         const bool is_orelay = (CG == 2) && (CL > 1) && !leader && warp == 2;
-        const bool is_arelay = false;  // (the peer's converter warps arrive on the leader directly)
-        if ((is_copier || is_orelay || is_arelay) && elect_one()) {
-            uint64_t* bars_r = is_orelay ? full_o : conv;
-            const uint32_t nst = static_cast<uint32_t>(is_arelay ? p.a_stages : p.o_stages);
+        if ((is_copier || is_orelay) && elect_one()) {
+            uint64_t* bars_r = full_o;
+            const uint32_t nst = static_cast<uint32_t>(p.o_stages);
             const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / CL);
             const uint32_t half_bytes = gen_rows * 128u;  // this CTA's share of one sub-tile
             const uint32_t half_off = pairq * half_bytes;
