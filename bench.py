@@ -337,6 +337,8 @@ def main():
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step as one CUDA graph (auto: on for 1 GPU when A < 1 GB, i.e. the "
                          "launch-latency-bound c1); per-phase times then come from a profiled eager pass")
+    ap.add_argument("--nccl-ar", action="store_true",
+                    help="AllReduce C with NCCL instead of the default fused NVLink peer-read sum (f1, symmetric memory)")
     ap.add_argument("--fused-rs", action="store_true",
                     help="f1: column / 2D layouts reduce-scatter partial B from the GEMM epilogue over NVLink "
                          "(symmetric memory) instead of NCCL reduce_scatter")
@@ -374,7 +376,8 @@ def main():
     peaks = load_peaks()
 
     local = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=args.mode, omega=args.omega, split_k=args.split_k)
-    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.fused_rs)
+    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.fused_rs,
+                    fused_ar=not args.nccl_ar)
     r0, r1, c0, c1 = ds.a_block_range()
     t_gen = time.perf_counter()
     A = make_A_block(W, args.workload, r0, r1, c0, c1, dev)
@@ -518,6 +521,7 @@ def main():
         "clocks": clocks,
         "comm": {"variant": args.variant if (W["nystrom"] and world > 1) else None,
                  "fused_reduce_scatter": bool(ds.fused_rs),
+                 "fused_allreduce": bool(ds.fused_ar and world > 1),
                  "predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"],
                                                                      args.variant if world > 1 else "noredist"),
                  "measured_bytes_per_rank": comm_bytes},

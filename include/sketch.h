@@ -139,6 +139,14 @@ sk_status_t sketch_apply_block_rs(sk_sketch_t h, const float* A_blk, int64_t m, 
 sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslots, int64_t slot_elems,
                                 int64_t rows, float* B, int64_t ldb, void* stream);
 
+/* out[i] = src[0][i] + src[1][i] + ... + src[n-1][i] (0 <= i < elems), summed in increasing j (fixed
+ * order, deterministic): the AllReduce of the Nystrom core's r x r partials (GPU
+ * variant P:1839) read straight from every rank's symmetric-memory slot over NVLink.
+ * src: n <= 8 device pointers valid in this process (e.g. NVLink peer mappings), 16-byte aligned;
+ * elems % 4 == 0.  Stream-ordered; the caller orders it after all ranks' writes (device barrier).
+ * Errors: SK_ERR_INVALID_VALUE, SK_ERR_SHAPE_MISMATCH, SK_ERR_ALIGNMENT. */
+sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, void* stream);
+
 /* Bytes of device workspace needed by sketch_apply / sketch_apply_block on n1 rows and
  * nystrom_core / core_apply_block (split-K partials of B and per-CTA r x r partials of C).
  * One size covers every entry point for that n1 (n for nystrom_core). */

@@ -746,6 +746,17 @@ sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslot
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "slot reduce launch");
 }
 
+sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, void* stream) {
+    if (!src || !out || n < 1 || n > 8 || elems < 0) return fail(SK_ERR_INVALID_VALUE, "bad peer sum");
+    if (elems & 3) return fail(SK_ERR_SHAPE_MISMATCH, "elems must be a multiple of 4");
+    for (int j = 0; j < n; ++j)
+        if (!src[j] || !aligned16(src[j])) return fail(SK_ERR_ALIGNMENT, "sources must be 16-byte aligned");
+    if (!aligned16(out)) return fail(SK_ERR_ALIGNMENT, "out must be 16-byte aligned");
+    if (elems == 0) return SK_SUCCESS;
+    cudaError_t e = sk::launch_sum_peers(src, n, elems, out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "peer sum launch");
+}
+
 sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb,
                              int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
                              void* stream) {

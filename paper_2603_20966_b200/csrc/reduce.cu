@@ -120,6 +120,33 @@ cudaError_t launch_streamk_reduce(const float* part, int64_t part_stride, int32_
     return cudaGetLastError();
 }
 
+// out[i] = sum_{j < n} src[j][i] in increasing j (fixed order): the AllReduce of C's r x r partials
+// read straight from every rank's symmetric-memory slot over NVLink.
+struct PeerPtrs {
+    const float4* p[8];
+};
+__global__ void sum_peers_kernel(PeerPtrs src, int32_t n, int64_t n4, float4* __restrict__ out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float4 acc = src.p[0][i];
+        for (int j = 1; j < n; ++j) {
+            const float4 v = src.p[j][i];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        out[i] = acc;
+    }
+}
+
+cudaError_t launch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, cudaStream_t s) {
+    if (n < 1 || n > 8 || (elems & 3)) return cudaErrorInvalidValue;
+    PeerPtrs pp{};
+    for (int j = 0; j < n; ++j) pp.p[j] = reinterpret_cast<const float4*>(src[j]);
+    const int64_t n4 = elems / 4;
+    const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 4));
+    sum_peers_kernel<<<std::max(blocks, 1), 256, 0, s>>>(pp, n, n4, reinterpret_cast<float4*>(out));
+    return cudaGetLastError();
+}
+
 // C[a, b] = sum_{c < chunks} part[c][a][b], r x nb, fixed order.
 __global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r, int32_t nb,
                                    float* __restrict__ C, int64_t ldc) {

@@ -94,7 +94,7 @@ class DistSketch:
 
     def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
                  mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128,
-                 fused_rs: bool = False):
+                 fused_rs: bool = False, fused_ar: bool = False):
         import torch.distributed as tdist
         self.tdist = tdist
         self.group = group
@@ -124,6 +124,9 @@ class DistSketch:
         # symmetric-memory receive buffers) instead of an NCCL reduce_scatter after the GEMM
         self.fused_rs = bool(fused_rs) and layout.p2 > 1
         self._rs = None
+        # f1: the AllReduce of C as one NVLink peer-read sum instead of NCCL (symmetric memory)
+        self.fused_ar = bool(fused_ar)
+        self._ar = None
 
     # ------------------------------------------------------------------ partition
     def a_block_range(self) -> tuple:
@@ -237,8 +240,37 @@ class DistSketch:
     def nystrom_core(self, A_blk):
         """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank."""
         Bp, (a, b) = self.apply(A_blk)
+        if self.world > 1 and self.fused_ar:
+            return Bp, (a, b), self._core_fused_allreduce(Bp, a)
         C = self.local.core_block(Bp, a)
         if self.world > 1:
             self.tdist.all_reduce(C, group=self.group)
             self.comm_bytes += C.numel() * 4
         return Bp, (a, b), C
+
+    def _core_fused_allreduce(self, Bp, a):
+        """AllReduce of the r x r core partials without NCCL: each rank's core GEMM
+        writes its partial into its own symmetric-memory slot (two slots, alternating per call), one
+        device barrier, then every rank sums all ranks' slots over NVLink in rank order."""
+        import torch
+        from . import sum_peers
+        r = self.r
+        if self._ar is None:
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = self.group if self.group is not None else self.tdist.group.WORLD
+            try:
+                symm_mem.enable_symm_mem_for_group(grp.group_name)
+            except Exception:  # pragma: no cover
+                pass
+            buf = symm_mem.empty((2, r * r), dtype=torch.float32, device=Bp.device)
+            hdl = symm_mem.rendezvous(buf, grp.group_name)
+            self._ar = {"buf": buf, "hdl": hdl, "ptrs": [int(x) for x in hdl.buffer_ptrs], "k": 0}
+        ar = self._ar
+        k = ar["k"]
+        ar["k"] ^= 1
+        self.local.core_block(Bp, a, out=ar["buf"][k].view(r, r))
+        ar["hdl"].barrier(channel=0)  # every rank's partial is in its slot k
+        C = torch.empty((r, r), dtype=torch.float32, device=Bp.device)
+        sum_peers([p + k * r * r * 4 for p in ar["ptrs"]], r * r, C)
+        self.comm_bytes += r * r * 4
+        return C

@@ -77,3 +77,54 @@ def test_fused_reduce_scatter_matches_nccl_and_oracle(spec, n1, n2, r):
         assert np.array_equal(Bn, Bf)
         assert np.array_equal(Bf.astype(np.float64), Bref[a:b])
         assert comm > 0
+
+
+def _worker_ar(rank, world, port, n, r, q):
+    import torch.distributed as tdist
+    import paper_2603_20966_b200 as sk
+    from inputs import synth
+    from paper_2603_20966_b200.dist import DistSketch, Layout
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+        out = {}
+        for fused in (False, True):
+            local = sk.Sketch(SEED, "rademacher", n, r, mode="tf32")
+            ds = DistSketch(SEED, "rademacher", n, n, r, Layout.parse("row", world), local=local, fused_ar=fused)
+            r0, r1, c0, c1 = ds.a_block_range()
+            Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1])).to(dev)
+            for _ in range(3):  # both alternating slots, then the first again
+                Bp, (a, b), C = ds.nystrom_core(Ablk)
+            torch.cuda.synchronize()
+            out[fused] = C.cpu().numpy()
+        q.put((rank, out))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_fused_allreduce_of_core_matches_nccl_and_oracle():
+    import torch.multiprocessing as mp
+    import oracle
+    from inputs import synth
+    world, n, r = 2, 2100, 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ar, args=(i, world, port, n, r, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+    _, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
+    for rank, out in res:
+        assert np.array_equal(out[False], out[True])
+        assert np.array_equal(out[True].astype(np.float64), Cref)
