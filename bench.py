@@ -339,9 +339,9 @@ def main():
                          "launch-latency-bound c1); per-phase times then come from a profiled eager pass")
     ap.add_argument("--nccl-ar", action="store_true",
                     help="AllReduce C with NCCL instead of the default fused NVLink peer-read sum (f1, symmetric memory)")
-    ap.add_argument("--fused-rs", action="store_true",
-                    help="f1: column / 2D layouts reduce-scatter partial B from the GEMM epilogue over NVLink "
-                         "(symmetric memory) instead of NCCL reduce_scatter")
+    ap.add_argument("--rs", default="peer", choices=["nccl", "peer", "epilogue"],
+                    help="reduce-scatter of partial B in column / 2D layouts: NCCL, symmetric-memory peer-read "
+                         "sum (default), or stores from the GEMM epilogue into the owners' slots (f1)")
     ap.add_argument("--omega-ablation", action="store_true",
                     help="f4: also time B = A*Omega with Omega materialised in HBM (+ all-gathered over NCCL "
                          "when N > 1) and a cuBLAS GEMM, against the fused in-kernel regeneration")
@@ -376,7 +376,7 @@ def main():
     peaks = load_peaks()
 
     local = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=args.mode, omega=args.omega, split_k=args.split_k)
-    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.fused_rs,
+    ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.rs,
                     fused_ar=not args.nccl_ar)
     r0, r1, c0, c1 = ds.a_block_range()
     t_gen = time.perf_counter()
@@ -520,7 +520,7 @@ def main():
         "cuda_graph": graph_info,
         "clocks": clocks,
         "comm": {"variant": args.variant if (W["nystrom"] and world > 1) else None,
-                 "fused_reduce_scatter": bool(ds.fused_rs),
+                 "reduce_scatter": ds.rs_mode,
                  "fused_allreduce": bool(ds.fused_ar and world > 1),
                  "predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"],
                                                                      args.variant if world > 1 else "noredist"),

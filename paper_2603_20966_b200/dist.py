@@ -94,7 +94,7 @@ class DistSketch:
 
     def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
                  mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128,
-                 fused_rs: bool = False, fused_ar: bool = False):
+                 fused_rs=False, fused_ar: bool = False):
         import torch.distributed as tdist
         self.tdist = tdist
         self.group = group
@@ -122,8 +122,19 @@ class DistSketch:
         self.comm_bytes = 0
         # f1: reduce-scatter of partial B fused into the GEMM epilogue (NVLink stores into the owners'
         # symmetric-memory receive buffers) instead of an NCCL reduce_scatter after the GEMM
-        self.fused_rs = bool(fused_rs) and layout.p2 > 1
+        # reduce-scatter of partial B for p2 > 1: False / "nccl" = NCCL reduce_scatter; "peer" = B-bar
+        # written into a symmetric-memory slot, one device barrier, each owner sums its piece from
+        # the p2 slots over NVLink in rank order; True / "epilogue" = the GEMM epilogue stores
+        # straight into the owners' slots
+        mode = {False: "nccl", None: "nccl", True: "epilogue"}.get(fused_rs, fused_rs)
+        if mode not in ("nccl", "peer", "epilogue"):
+            raise ValueError(f"unknown reduce-scatter mode {fused_rs!r}")
+        if mode == "peer" and r % 4:
+            mode = "nccl"  # the peer-read sum works on float4
+        self.rs_mode = mode if layout.p2 > 1 else "nccl"
+        self.fused_rs = self.rs_mode != "nccl"
         self._rs = None
+        self._rsp = None
         # f1: the AllReduce of C as one NVLink peer-read sum instead of NCCL (symmetric memory)
         self.fused_ar = bool(fused_ar)
         self._ar = None
@@ -154,14 +165,47 @@ class DistSketch:
             return self.local.apply_block(A_blk, c0), (r0, r1)
         rows = r1 - r0
         per = -(-rows // p2)
-        if self.fused_rs:
+        if self.rs_mode == "epilogue":
             return self._apply_fused_rs(A_blk, rows, per, c0)
+        if self.rs_mode == "peer":
+            return self._apply_peer_rs(A_blk, rows, per, c0)
         Bbar = torch.zeros((per * p2, self.r), dtype=torch.float32, device=A_blk.device)
         self.local.apply_block(A_blk, c0, out=Bbar[:rows])
         piece = torch.empty((per, self.r), dtype=torch.float32, device=A_blk.device)
         self.tdist.reduce_scatter_tensor(piece, Bbar, group=self.row_group)
         self.comm_bytes += Bbar.numel() * 4 * (p2 - 1) // p2
         a, b = self.b_piece_rows()
+        return piece[: b - a], (a, b)
+
+    def _apply_peer_rs(self, A_blk, rows, per, c0):
+        """Alg. 1 line 415 over symmetric memory: B-bar (rows padded to p2 * per) is written into this
+        rank's slot (two slots alternating per call), one device barrier over the row group, then the
+        owner of piece j sums rows [j per, (j+1) per) of the p2 slots over NVLink in rank order."""
+        import torch
+        from . import sum_peers
+        p2, r = self.layout.p2, self.r
+        key = (rows, per)
+        if self._rsp is None or self._rsp["key"] != key:
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = self.row_group if self.row_group is not None else self.tdist.group.WORLD
+            try:
+                symm_mem.enable_symm_mem_for_group(grp.group_name)
+            except Exception:  # pragma: no cover
+                pass
+            buf = symm_mem.empty((2, p2 * per, r), dtype=torch.float32, device=A_blk.device)
+            buf.zero_()  # padding rows of the last piece stay zero
+            hdl = symm_mem.rendezvous(buf, grp.group_name)
+            self._rsp = {"key": key, "buf": buf, "hdl": hdl, "ptrs": [int(x) for x in hdl.buffer_ptrs], "k": 0}
+        st = self._rsp
+        k = st["k"]
+        st["k"] ^= 1
+        self.local.apply_block(A_blk, c0, out=st["buf"][k][:rows])
+        st["hdl"].barrier(channel=0)  # every rank's B-bar is in its slot k
+        a, b = self.b_piece_rows()
+        piece = torch.empty((per, r), dtype=torch.float32, device=A_blk.device)
+        off = (k * p2 * per + self.j * per) * r * 4
+        sum_peers([p + off for p in st["ptrs"]], per * r, piece)
+        self.comm_bytes += 4 * per * r * (p2 - 1)
         return piece[: b - a], (a, b)
 
     def _apply_fused_rs(self, A_blk, rows, per, c0):

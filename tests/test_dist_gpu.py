@@ -1,8 +1,8 @@
 """Multi-GPU layouts on real GPUs (needs >= 2 CUDA devices; skipped otherwise).
 
-The fused reduce-scatter (partial B stored from the GEMM epilogue into the owners'
-symmetric-memory receive slots over NVLink, then a fixed-order slot sum) must return exactly the
-B pieces of the NCCL reduce_scatter path in the integer regime (integer A, Rademacher Omega: every
+The fused reduce-scatters (partial B stored from the GEMM epilogue into the owners'
+symmetric-memory receive slots over NVLink, or written locally and summed by the owners with NVLink
+peer reads; both fixed-order) must return exactly the B pieces of the NCCL reduce_scatter path in the integer regime (integer A, Rademacher Omega: every
 partial sum is exact in fp32), and those must equal the oracle's."""
 import os
 import socket
@@ -36,7 +36,7 @@ def _worker(rank, world, port, spec, n1, n2, r, q):
         layout = Layout.parse(spec, world)
         A = synth.int_matrix(7, n1, n2, -4, 4)
         out = {}
-        for fused in (False, True):
+        for fused in ("nccl", "epilogue", "peer"):
             local = sk.Sketch(SEED, "rademacher", n2, r, mode="tf32")
             ds = DistSketch(SEED, "rademacher", n1, n2, r, layout, local=local, fused_rs=fused)
             r0, r1, c0, c1 = ds.a_block_range()
@@ -71,12 +71,13 @@ def test_fused_reduce_scatter_matches_nccl_and_oracle(spec, n1, n2, r):
     A = synth.int_matrix(7, n1, n2, -4, 4)
     Bref = oracle.sketch(SEED, "rademacher", A, r)
     for rank, out in res:
-        a, b, Bn, _ = out[False]
-        af, bf, Bf, comm = out[True]
-        assert (a, b) == (af, bf)
-        assert np.array_equal(Bn, Bf)
-        assert np.array_equal(Bf.astype(np.float64), Bref[a:b])
-        assert comm > 0
+        a, b, Bn, _ = out["nccl"]
+        for mode in ("epilogue", "peer"):
+            af, bf, Bf, comm = out[mode]
+            assert (a, b) == (af, bf)
+            assert np.array_equal(Bn, Bf), mode
+            assert np.array_equal(Bf.astype(np.float64), Bref[a:b]), mode
+            assert comm > 0
 
 
 def _worker_ar(rank, world, port, n, r, q):
