@@ -168,7 +168,10 @@ class DistSketch:
         if self.rs_mode == "epilogue":
             return self._apply_fused_rs(A_blk, rows, per, c0)
         if self.rs_mode == "peer":
-            return self._apply_peer_rs(A_blk, rows, per, c0)
+            try:
+                return self._apply_peer_rs(A_blk, rows, per, c0)
+            except Exception as e:  # symmetric memory unavailable: NCCL from now on (same results)
+                self._fallback("peer-read reduce-scatter", e)
         Bbar = torch.zeros((per * p2, self.r), dtype=torch.float32, device=A_blk.device)
         self.local.apply_block(A_blk, c0, out=Bbar[:rows])
         piece = torch.empty((per, self.r), dtype=torch.float32, device=A_blk.device)
@@ -176,6 +179,14 @@ class DistSketch:
         self.comm_bytes += Bbar.numel() * 4 * (p2 - 1) // p2
         a, b = self.b_piece_rows()
         return piece[: b - a], (a, b)
+
+    def _fallback(self, what, err):
+        """Symmetric memory could not be set up (every rank hits the same condition): use NCCL."""
+        import sys
+        print(f"[dist] {what} over symmetric memory unavailable ({err!r}); using NCCL", file=sys.stderr)
+        if self.rs_mode in ("peer", "epilogue"):
+            self.rs_mode, self.fused_rs = "nccl", False
+        self.fused_ar = False
 
     def _apply_peer_rs(self, A_blk, rows, per, c0):
         """Alg. 1 line 415 over symmetric memory: B-bar (rows padded to p2 * per) is written into this
@@ -285,7 +296,10 @@ class DistSketch:
         """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank."""
         Bp, (a, b) = self.apply(A_blk)
         if self.world > 1 and self.fused_ar:
-            return Bp, (a, b), self._core_fused_allreduce(Bp, a)
+            try:
+                return Bp, (a, b), self._core_fused_allreduce(Bp, a)
+            except Exception as e:  # symmetric memory unavailable: NCCL from now on (same results)
+                self._fallback("fused AllReduce", e)
         C = self.local.core_block(Bp, a)
         if self.world > 1:
             self.tdist.all_reduce(C, group=self.group)
