@@ -237,7 +237,8 @@ def run_reference(args, W, wl_name):
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": W["desc"], "sample_rows": rows},
+        "config": {"workload": W["desc"], "n1": W["n1"], "n2": W["n2"], "r": W["r"], "dist": W["dist"],
+                   "mode": "f64 oracle", "layout": "host", "sample_rows": rows},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
