@@ -106,7 +106,10 @@ __device__ __forceinline__ float2 cos_sin_2pi(uint32_t a) {
 
 __device__ __forceinline__ float2 box_muller_accurate(uint32_t w1, uint32_t w2) {
     const float u1 = __uint2float_rn((w1 >> 8) + 1u) * 0x1p-24f;  // (0,1], exact
-    const float R = sqrtf(2.0f * neg_log_u1(u1));
+    // sqrt.rn (correctly rounded) with flush-to-zero: the argument is >= 2^-23 (never subnormal), so
+    // the result is bit-identical to sqrtf without the subnormal-input slow path
+    float R;
+    asm("sqrt.rn.ftz.f32 %0, %1;" : "=f"(R) : "f"(2.0f * neg_log_u1(u1)));
     const float2 cs = cos_sin_2pi(w2 >> 8);
     return make_float2(R * cs.x, R * cs.y);
 }
