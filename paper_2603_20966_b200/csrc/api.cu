@@ -203,10 +203,19 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // shared bytes (6.2 -> 7.1 ms with sharing); then 2 pairs, then none if the shape does not allow
     // it.  sketch_set_cta_group(h, 2 / 4 / 8) forces none / 2 pairs / 4 pairs.
     auto cl_ok = [&](int cl) {
-        return P.cg == 2 && P.nacc == 2 && n1 >= 512 * cl && npad_max % (16 * cl) == 0 && h->dist == sk::kGaussian;
+        // every pair generates whole 8-row swizzle atoms of each CTA's npad/2-row Omega slice
+        const bool split_ok = (cl == 3) ? (npad_max % 16 == 0 && npad_max / 16 >= cl) : (npad_max % (16 * cl) == 0);
+        return P.cg == 2 && P.nacc == 2 && n1 >= 512 * cl && split_ok && h->dist == sk::kGaussian;
     };
     P.cl = 1;
-    if (h->cl_override == 0 && !x3) P.cl = cl_ok(4) ? 4 : cl_ok(2) ? 2 : 1;
+    // bf16 with the fast (MUFU) transform generates Omega cheaply enough that 3 pairs per cluster
+    // win: clusters of 6 CTAs pack 22 per B200 (132 SMs) against 15 of 8 CTAs (120 SMs), at 4/3
+    // the generated elements per A byte (c2: 2.00 -> 1.92 ms, 25000^2: 0.537 -> 0.510 ms; the
+    // accurate transform loses, 2.11 -> 2.22 ms).  Only for n1 >= 16 units of 1536 rows, so the
+    // ragged last unit stays a small share (c4, n1 = 2048, keeps one 2048-row unit).
+    const bool fast = h->omega_transform == SK_OMEGA_FAST;
+    if (h->cl_override == 0 && !x3)
+        P.cl = (bf && fast && n1 >= 16 * 1536 && cl_ok(3)) ? 3 : cl_ok(4) ? 4 : cl_ok(2) ? 2 : 1;
     else if (h->cl_override >= 2) P.cl = cl_ok(h->cl_override) ? h->cl_override : 1;
     int workers = sk::num_sms() / P.cg;
     if (P.cl > 1) {
@@ -624,10 +633,10 @@ sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k) {
 
 sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    if (!(cg == 0 || cg == 1 || cg == 2 || cg == 4 || cg == 8))
-        return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1, 2, 4 or 8");
-    h->cg_override = (cg >= 4) ? 0 : cg;                                 // 4 / 8: pairs + sharing
-    h->cl_override = (cg == 2) ? 1 : (cg == 4) ? 2 : (cg == 8) ? 4 : 0;  // 2: pairs, no sharing
+    if (!(cg == 0 || cg == 1 || cg == 2 || cg == 4 || cg == 6 || cg == 8))
+        return fail(SK_ERR_INVALID_VALUE, "cta group must be 0 (auto), 1, 2, 4, 6 or 8");
+    h->cg_override = (cg >= 4) ? 0 : cg;                // 4 / 6 / 8: pairs + sharing
+    h->cl_override = (cg == 2) ? 1 : (cg >= 4) ? cg / 2 : 0;  // 2: pairs, no sharing
     return SK_SUCCESS;
 }
 

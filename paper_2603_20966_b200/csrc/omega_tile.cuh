@@ -16,6 +16,11 @@ namespace sk {
 // (Omega rows kglob0 .. kglob0+31), K-major SW128: byte n*128 + ((j4 ^ (n&7)) << 4) + 4*e.
 // kglob0 = 128-aligned base + 32*kit + roff, roff in {0,1,2,3} (roff != 0 only for block calls
 // whose k0 is not a multiple of 4: then each 4-row chunk straddles two Philox calls).
+// SWIZZLE_128B phase of the 128-B row at shared address `row`: address bits 7..9 (the tiles are
+// 1024-B aligned, so this is n & 7 of the tile row; it also holds for a writer whose share of the
+// tile starts at a row that is not a multiple of 8, as with clusters of 3 pairs)
+__device__ __forceinline__ uint32_t sw128_phase(uint32_t row) { return (row >> 7) & 7u; }
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, float4 v) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w)
@@ -58,7 +63,7 @@ __device__ __forceinline__ void produce_omega_tile_r(uint8_t* tile, int64_t kglo
     const int n = t;
     const uint32_t col = static_cast<uint32_t>(c0 + n);
     const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
-    const uint32_t sw = static_cast<uint32_t>(n & 7);
+    const uint32_t sw = sw128_phase(row_base);
     {
         // bits for tile rows kk = 0..31: global rows kglob0 + kk
         const uint64_t g = static_cast<uint64_t>(kglob0);
@@ -102,11 +107,12 @@ __device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglo
             const uint4 xb = philox_gauss_call(q0 + j2c, static_cast<uint32_t>(c0 + n2c), key0, key1);
             const float4 va = values4<DIST, FAST>(xa);
             const float4 vb = values4<DIST, FAST>(xb);
-            store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n) * 128u +
-                                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4), va, lo_off);
-            if (two)
-                store_chunk<DIST, MODE, FAST>(tile_base + static_cast<uint32_t>(n2) * 128u +
-                                                  ((static_cast<uint32_t>(j2) ^ static_cast<uint32_t>(n2 & 7)) << 4), vb, lo_off);
+            const uint32_t ra = tile_base + static_cast<uint32_t>(n) * 128u;
+            store_chunk<DIST, MODE, FAST>(ra + ((static_cast<uint32_t>(j4) ^ sw128_phase(ra)) << 4), va, lo_off);
+            if (two) {
+                const uint32_t rb = tile_base + static_cast<uint32_t>(n2) * 128u;
+                store_chunk<DIST, MODE, FAST>(rb + ((static_cast<uint32_t>(j2) ^ sw128_phase(rb)) << 4), vb, lo_off);
+            }
             n = n2 + tr;
             j4 = j2 + tq;
             if (n >= npad) { n -= npad; ++j4; }
@@ -116,8 +122,8 @@ __device__ __forceinline__ void produce_omega_tile_g(uint8_t* tile, int64_t kglo
 #pragma unroll 1
     for (; j4 < 8;) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
-        const uint32_t addr = tile_base + static_cast<uint32_t>(n) * 128u +
-                              ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(n & 7)) << 4);
+        const uint32_t ra = tile_base + static_cast<uint32_t>(n) * 128u;
+        const uint32_t addr = ra + ((static_cast<uint32_t>(j4) ^ sw128_phase(ra)) << 4);
         // rows 4(q0+j4)+roff .. +3: tail of call q0+j4, head of call q0+j4+1
         const float4 a0 = values4<DIST, FAST>(philox_gauss_call(q0 + j4, col, key0, key1));
         const float4 a1 = values4<DIST, FAST>(philox_gauss_call(q0 + j4 + 1, col, key0, key1));
@@ -147,7 +153,7 @@ __device__ __forceinline__ void produce_omega_tile_bf16_r(uint8_t* tile, int64_t
     const int n = t;
     const uint32_t col = static_cast<uint32_t>(c0 + n);
     const uint32_t row_base = smem_u32(tile) + static_cast<uint32_t>(n) * 128u;
-    const uint32_t sw = static_cast<uint32_t>(n & 7);
+    const uint32_t sw = sw128_phase(row_base);
     // 64 bits for rows kglob0 .. kglob0 + 63, bit b of the 64 = row kglob0 + b
     const uint64_t g = static_cast<uint64_t>(kglob0);
     const uint4 x = philox_rade_call(g >> 7, col, key0, key1);
@@ -194,7 +200,7 @@ __device__ __forceinline__ void produce_omega_tile_bf16_g(uint8_t* tile, int64_t
     while (j < kJ) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
         const uint32_t row = tile_base + static_cast<uint32_t>(n) * 128u;
-        const uint32_t sw = static_cast<uint32_t>(n & 7);
+        const uint32_t sw = sw128_phase(row);
         if constexpr (HALF) {
             const float4 a = values4<DIST, FAST>(philox_gauss_call(q0 + j, col, key0, key1));
             float v[4] = {a.x, a.y, a.z, a.w};

@@ -133,7 +133,7 @@ template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1>
 __global__ void __launch_bounds__(threads_for(MODE), 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
     static_assert(CL == 1 || CG == 2, "Omega sharing between pairs needs CTA pairs");
-    static_assert(CL == 1 || CL == 2 || CL == 4, "1, 2 or 4 CTA pairs per cluster");
+    static_assert(CL >= 1 && CL <= 4, "1 to 4 CTA pairs per cluster");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -222,6 +222,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int rows_per_unit = 128 * CG * NACC * CL;   // rows of a work unit (all pairs of a cluster)
+    // pair q of the cluster generates Omega slice rows [share(q), share(q+1)), as even as rows
+    // allow (CL = 3: 42/43/43 of 128; the tile writers take the swizzle phase from the address)
+    auto omega_share_row0 = [](int rows, uint32_t q) {
+        return static_cast<int>((static_cast<uint32_t>(rows) * q) / static_cast<uint32_t>(CL));
+    };
     const int pair_row0 = static_cast<int>(pairq) * 128 * CG * NACC;  // this pair's rows inside a unit
 
     if (warp == 0) {
@@ -371,10 +376,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         if ((is_copier || is_orelay) && elect_one()) {
             uint64_t* bars_r = full_o;
             const uint32_t nst = static_cast<uint32_t>(p.o_stages);
-            const uint32_t gen_rows = static_cast<uint32_t>(npad_loc / CL);
+            const uint32_t gen_rows = static_cast<uint32_t>(omega_share_row0(npad_loc, pairq + 1) -
+                                                            omega_share_row0(npad_loc, pairq));
             const uint32_t half_bytes = gen_rows * 128u;  // this CTA's share of one sub-tile
-            const uint32_t half_off = pairq * half_bytes;
-            const uint32_t tx = half_bytes * (OLO ? 2u : 1u) * NSUBO * (CL - 1);
+            const uint32_t half_off = static_cast<uint32_t>(omega_share_row0(npad_loc, pairq)) * 128u;
+            // the partners' shares land here: all rows of the slice but this CTA's own
+            const uint32_t tx = (static_cast<uint32_t>(npad_loc) - gen_rows) * 128u * (OLO ? 2u : 1u) * NSUBO;
             uint32_t st = 0, ph = 0, ntr = 0;
             WorkIter wi(p, group);
             int mb, kb, ke, s;
@@ -413,8 +420,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     } else if (warp >= kCtlWarps && warp < kCtlWarps + kRngW) {
         // ------------------------------------------------------------------ Omega producers + epilogue
         const int t = static_cast<int>(threadIdx.x) - kCtlWarps * 32;
-        const int gen_rows = npad_loc / CL;                                      // rows this CTA generates
-        const int gen_row0 = static_cast<int>(pairq) * gen_rows;                 // first generated row
+        const int gen_row0 = omega_share_row0(npad_loc, pairq);                  // first generated row
+        const int gen_rows = omega_share_row0(npad_loc, pairq + 1) - gen_row0;   // rows this CTA generates
         // tf32 64-K stages hold two 32-K sub-tiles: when one sub-tile has at most half as many
         // chunks as there are producers (clusters of 4 pairs), each half of the producers takes one
         // sub-tile instead of both halves idling through the sub-tiles in turn
@@ -662,8 +669,8 @@ int sketch_gemm_max_smem() { return 227 * 1024; }
 // Clusters of `cluster` CTAs of this kernel that can be co-resident (GPC packing strands SMs for
 // clusters of 4).  Returns 0 if the query fails.
 int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem) {
-    static int cache[3][4][2] = {};  // [cl/2][mode][fast] + 1, per process
-    const int ci = cl == 4 ? 2 : 1;
+    static int cache[5][4][2] = {};  // [cl][mode][fast] + 1, per process
+    const int ci = cl >= 1 && cl <= 4 ? cl : 0;
     if (mode >= 0 && mode < 4 && cache[ci][mode][fast ? 1 : 0] > 0) return cache[ci][mode][fast ? 1 : 0] - 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cg * cl * 64);
@@ -683,6 +690,10 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
         if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 2); else SK_FN(kTF32, false, 2); }
         else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 2); else SK_FN(kBF16, false, 2); }
         else SK_FN(kTF32x3, false, 2);
+    } else if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 3) {
+        if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 3); else SK_FN(kTF32, false, 3); }
+        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 3); else SK_FN(kBF16, false, 3); }
+        else SK_FN(kTF32x3, false, 3);
     } else if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 4) {
         if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 4); else SK_FN(kTF32, false, 4); }
         else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 4); else SK_FN(kBF16, false, 4); }
@@ -751,6 +762,7 @@ cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p
                                int dist, int mode, bool fast, int grid, size_t smem,
                                cudaStream_t s, int cl) {
     if (cl == 4 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 4>(tmA, p, dist, mode, fast, grid, smem, s);
+    if (cl == 3 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 3>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cl == 2 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cl == 2 && cg == 2 && nacc == 1) return dispatch_dist<2, 1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
     if (cg == 1 && nacc == 1) return dispatch_dist<1, 1>(tmA, p, dist, mode, fast, grid, smem, s);
