@@ -324,7 +324,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="bf16", choices=["tf32", "tf32x3", "bf16"])
-    ap.add_argument("--omega", default="accurate", choices=["accurate", "fast"])
+    ap.add_argument("--omega", default="auto", choices=["auto", "accurate", "fast"],
+                    help="Gaussian transform: auto = fast (MUFU Box-Muller, error <= 2^-16 max(|z|,1)) in bf16 "
+                         "mode, whose RN rounding of Omega to bf16 (2^-9) hides it (same relF of B as accurate), "
+                         "accurate (<= 2 ulp fp32) in tf32 / tf32x3 (reading R5)")
     ap.add_argument("--layout", default="auto",
                     help="row | col | AxB (p1 x p2) | auto = the layout BASELINE.json names for the workload "
                          "(c2: 2D grid, c3: row-block, c4: column-block)")
@@ -353,6 +356,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args, W, args.workload)
     args.warmup = max(args.warmup, 3)
+    if args.omega == "auto":
+        args.omega = "fast" if args.mode == "bf16" else "accurate"
 
     import numpy as np
     import torch
