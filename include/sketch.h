@@ -91,7 +91,7 @@ sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k);
  * tcgen05 cta_group::2 for n1 > 256; in bf16 mode, clusters of two pairs sharing the generated
  * Gaussian Omega slices for n1 >= 2048), 1 = single-CTA tiles, 2 = CTA pairs without sharing,
  * 4 = clusters of 2 pairs sharing Omega whenever the shape allows it (any mode), 6 = clusters of 3
- * pairs (6 CTAs; the automatic choice for bf16 with SK_OMEGA_FAST at n1 >= 24576), 8 = clusters of 4
+ * pairs (6 CTAs; the automatic choice for bf16 with SK_OMEGA_FAST at n1 >= 6144), 8 = clusters of 4
  * pairs (8 CTAs) sharing Omega.  Any other value: SK_ERR_INVALID_VALUE. */
 sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg);
 
