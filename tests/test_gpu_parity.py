@@ -424,3 +424,28 @@ def test_streamk_matches_oracle(dist, mode, capfd, monkeypatch):
         assert np.array_equal(got.astype(np.float64), ref)
     else:
         assert _relF(got, ref) <= TOL[mode]
+
+
+# ----------------------------------------------------------------------------- clusters of 3 CTA pairs
+@pytest.mark.parametrize("r", [48, 80, 200, 256])
+def test_three_pair_clusters_auto(r, capfd, monkeypatch):
+    """bf16 + fast transform at n1 >= 6144 runs clusters of 3 pairs automatically; each pair
+    generates an uneven share of the Omega slice (r = 80: 13/13/14 of 40 rows, starting off the
+    8-row swizzle atom).  B matches the oracle, and equals the unshared CTA pairs bit for bit (same
+    split-K, so the same MMA sequence per row); a ragged last unit (6200 rows) is covered."""
+    sk = _sk()
+    monkeypatch.setenv("SK_DEBUG_PLAN", "1")
+    n1, n2 = 6200, 1500
+    A = synth.uniform(27, n1, n2)
+    Ad = _dev(A)
+    s = sk.Sketch(SEED, "gaussian", n2, r, mode="bf16", omega="fast", split_k=2)
+    B = s.apply(Ad)
+    torch.cuda.synchronize()
+    err = capfd.readouterr().err
+    plans = [l for l in err.splitlines() if l.startswith("[sketch plan]") and f"n1={n1}" in l]
+    assert plans and all(" cl=3 " in l for l in plans), plans[:2]
+    ref_pairs = sk.Sketch(SEED, "gaussian", n2, r, mode="bf16", omega="fast", split_k=2, cta_group=2).apply(Ad)
+    assert torch.equal(B, ref_pairs)
+    rows = np.concatenate([np.arange(0, 40), np.linspace(40, n1 - 1, 40).astype(int), np.arange(n1 - 30, n1)])
+    ref = oracle.sketch(SEED, "gaussian", A[rows].astype(np.float64), r)
+    assert _relF(B.cpu().numpy()[rows], ref) <= TOL["bf16"]
