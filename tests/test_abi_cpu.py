@@ -41,6 +41,11 @@ def test_host_validation_without_gpu():
     try:
         assert lib.sketch_set_mode(h, 9) == 1
         assert lib.sketch_set_split_k(h, 65) == 1
+        # CTA grouping override: 0 / 1 / 2 / 4 / 6 / 8 (clusters of 0..4 pairs), anything else rejected
+        for cg in (0, 1, 2, 4, 6, 8):
+            assert lib.sketch_set_cta_group(h, cg) == 0
+        for cg in (3, 5, 7, 16, -1):
+            assert lib.sketch_set_cta_group(h, cg) == 1
         n = ctypes.c_size_t()
         assert lib.sketch_workspace_size(h, 5000, ctypes.byref(n)) == 0
         # shape mismatch is reported before any device work
