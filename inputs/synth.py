@@ -79,6 +79,20 @@ def uniform_device(seed: int, n1: int, n2: int, device="cuda", out=None):
     return out
 
 
+def int_matrix_device(seed: int, n1: int, n2: int, lo: int = -4, hi: int = 4, device="cuda", out=None):
+    """iid integers in [lo, hi] as fp32, generated in HBM in row chunks (full-size integer-regime tests)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    if out is None:
+        out = torch.empty((n1, n2), dtype=torch.float32, device=device)
+    step = max(1, (1 << 27) // max(n2, 1))
+    for i in range(0, n1, step):
+        blk = out[i:i + step]
+        blk.copy_(torch.randint(lo, hi + 1, blk.shape, generator=g, device=device, dtype=torch.int32))
+    return out
+
+
 def rbf_kernel_device(seed: int, n: int, d: int, device="cuda", out=None, chunk: int = 8192):
     """RBF kernel of X ~ U[0,1)^{n x d} built in row blocks on the GPU (fp64 distances)."""
     import torch
