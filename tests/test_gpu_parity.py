@@ -449,3 +449,26 @@ def test_three_pair_clusters_auto(r, capfd, monkeypatch):
     rows = np.concatenate([np.arange(0, 40), np.linspace(40, n1 - 1, 40).astype(int), np.arange(n1 - 30, n1)])
     ref = oracle.sketch(SEED, "gaussian", A[rows].astype(np.float64), r)
     assert _relF(B.cpu().numpy()[rows], ref) <= TOL["bf16"]
+
+
+@pytest.mark.parametrize("k0", [1, 333, 25000])
+def test_three_pair_clusters_block_offsets(k0, capfd, monkeypatch):
+    """The 2D-grid block form on clusters of 3 pairs (bf16 / fast, n1 >= 6144): a block of A whose
+    column 0 is Omega row k0 (unaligned k0 makes every 4-row Philox chunk straddle two calls) matches
+    the oracle on sampled rows and equals the unshared pairs bit for bit."""
+    sk = _sk()
+    monkeypatch.setenv("SK_DEBUG_PLAN", "1")
+    n1, k, r = 6400, 900, 256
+    A = synth.uniform(29, n1, k)
+    Ad = _dev(A)
+    s = sk.Sketch(SEED, "gaussian", 40000, r, mode="bf16", omega="fast", split_k=1)
+    Bp = s.apply_block(Ad, k0)
+    torch.cuda.synchronize()
+    plans = [l for l in capfd.readouterr().err.splitlines() if l.startswith("[sketch plan]") and f"n1={n1}" in l]
+    assert plans and all(" cl=3 " in l for l in plans), plans[:2]
+    ref_pairs = sk.Sketch(SEED, "gaussian", 40000, r, mode="bf16", omega="fast", split_k=1,
+                          cta_group=2).apply_block(Ad, k0)
+    assert torch.equal(Bp, ref_pairs)
+    rows = np.concatenate([np.arange(0, 16), np.linspace(16, n1 - 1, 32).astype(int)])
+    ref = oracle.sketch(SEED, "gaussian", A[rows], r, k0=k0)
+    assert _relF(Bp.cpu().numpy()[rows], ref) <= TOL["bf16"]
