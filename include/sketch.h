@@ -148,6 +148,16 @@ sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslot
  * Errors: SK_ERR_INVALID_VALUE, SK_ERR_SHAPE_MISMATCH, SK_ERR_ALIGNMENT. */
 sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, void* stream);
 
+/* Pack of the Redist variant's All-to-All ("unpack" step PAPER.md:1536): for column
+ * bounds cb[0] = 0 < cb[1] < ... < cb[nblk] <= ldb, writes block j = B[0:rows, cb[j]:cb[j+1]]
+ * row-major and contiguous at out + rows * cb[j] (out holds rows * cb[nblk] floats), so that each
+ * rank's send chunk is one contiguous range.  B: device, row-major, ldb >= cb[nblk]; cb: HOST array
+ * of nblk + 1 bounds; 1 <= nblk <= 64.  Pure data movement (no arithmetic).  Stream-ordered.
+ * Errors: SK_ERR_INVALID_VALUE (NULL pointers, nblk, non-increasing bounds),
+ * SK_ERR_SHAPE_MISMATCH (cb[nblk] > ldb). */
+sk_status_t sketch_pack_cols(const float* B, int64_t rows, int64_t ldb, const int64_t* cb, int32_t nblk,
+                             float* out, void* stream);
+
 /* Bytes of device workspace needed by sketch_apply / sketch_apply_block on n1 rows and
  * nystrom_core / core_apply_block (split-K partials of B and per-CTA r x r partials of C).
  * One size covers every entry point for that n1 (n for nystrom_core). */

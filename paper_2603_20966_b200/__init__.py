@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation", "sketch_set_trace",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
-    "sketch_rs_split", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers",
+    "sketch_rs_split", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers", "sketch_pack_cols",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
@@ -87,6 +87,7 @@ def load_library(build_if_missing: bool = True):
                                               i32, vp]
         lib.sketch_reduce_slots.argtypes = [vp, vp, i32, i64, i64, vp, i64, vp]
         lib.sketch_sum_peers.argtypes = [ctypes.POINTER(vp), i32, i64, vp, vp]
+        lib.sketch_pack_cols.argtypes = [vp, i64, i64, ctypes.POINTER(i64), i32, vp, vp]
         lib.sketch_set_trace.argtypes = [vp, vp, i32]
         lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
         lib.sketch_generate_bits.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
@@ -307,6 +308,20 @@ class Sketch:
         _check(self._lib.core_apply_block_cols(self._h, B_blk.data_ptr(), m, nb, B_blk.stride(0), int(i0),
                                                out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
                                                _stream_ptr(stream)))
+        return out
+
+    def pack_cols(self, B_blk, col_bounds, out=None, stream=None):
+        """Column blocks of B_blk packed back to back (Redist All-to-All send buffer, sketch_pack_cols)."""
+        torch = _torch()
+        _require_cuda(B_blk, out)
+        rows = B_blk.shape[0]
+        nblk = len(col_bounds) - 1
+        if out is None:
+            out = torch.empty(rows * int(col_bounds[-1]), dtype=torch.float32, device=B_blk.device)
+        cb = (ctypes.c_int64 * len(col_bounds))(*[int(x) for x in col_bounds])
+        _check(self._lib.sketch_pack_cols(ctypes.c_void_p(B_blk.data_ptr()), ctypes.c_int64(rows),
+                                          ctypes.c_int64(B_blk.stride(0) if rows else 1), cb, ctypes.c_int32(nblk),
+                                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
     def nystrom_core(self, A, B=None, C=None, stream=None):

@@ -767,6 +767,19 @@ sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, 
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "peer sum launch");
 }
 
+sk_status_t sketch_pack_cols(const float* B, int64_t rows, int64_t ldb, const int64_t* cb, int32_t nblk,
+                             float* out, void* stream) {
+    if (!cb || nblk < 1 || nblk > 64 || rows < 0) return fail(SK_ERR_INVALID_VALUE, "bad column-pack arguments");
+    if (cb[0] != 0) return fail(SK_ERR_INVALID_VALUE, "cb[0] must be 0");
+    for (int j = 0; j < nblk; ++j)
+        if (cb[j + 1] < cb[j]) return fail(SK_ERR_INVALID_VALUE, "column bounds must be non-decreasing");
+    if (cb[nblk] > ldb) return fail(SK_ERR_SHAPE_MISMATCH, "cb[nblk] > ldb");
+    if (rows == 0 || cb[nblk] == 0) return SK_SUCCESS;
+    if (!B || !out) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    cudaError_t e = sk::launch_pack_cols(B, rows, ldb, cb, nblk, out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "pack_cols launch");
+}
+
 sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb,
                              int64_t i0, float* C_part, int64_t ldc, void* ws, size_t ws_bytes,
                              void* stream) {

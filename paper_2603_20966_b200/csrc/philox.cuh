@@ -114,26 +114,43 @@ __device__ __forceinline__ float2 box_muller_accurate(uint32_t w1, uint32_t w2) 
     return make_float2(R * cs.x, R * cs.y);
 }
 
-// Box-Muller on the MUFU special-function unit (lg2 / sqrt / sin / cos .approx); allowed only
-// in the tf32 / bf16 modes, whose operand rounding (2^-11 / 2^-8) dominates its error
-// (reading R5).  The angle is centred to [-pi, pi) before sin/cos.approx.
+// (cos 2 pi u2, sin 2 pi u2) on the MUFU special-function unit: the same exact quarter-turn
+// reduction in integers as cos_sin_2pi (rem in [-2^21, 2^21), exact), so the MUFU only ever sees
+// |theta| <= pi/4 and the rotation by q quarter turns is exact -- sin/cos of 0 are exactly 0 / 1,
+// which gives the exact zeros at u2 in {0, 1/4, 1/2, 3/4} (reading R14).  theta = rem * pi 2^-23
+// is rounded once (relative 2^-24).
+__device__ __forceinline__ float2 cos_sin_2pi_fast(uint32_t a) {
+    const uint32_t qa = (a + (1u << 21)) >> 22;
+    const uint32_t q = qa & 3u;
+    const int32_t rem = static_cast<int32_t>(a) - static_cast<int32_t>(qa << 22);
+    const float th = __int2float_rn(rem) * (3.14159265358979323846f * 0x1p-23f);
+    float sn, cs;
+    asm("sin.approx.f32 %0, %1;" : "=f"(sn) : "f"(th));
+    asm("cos.approx.f32 %0, %1;" : "=f"(cs) : "f"(th));
+    const float c0 = (q & 1u) ? sn : cs;
+    const float s0 = (q & 1u) ? cs : sn;
+    const uint32_t negc = ((q + 1u) & 2u) << 30;  // q = 1, 2
+    const uint32_t negs = (q & 2u) << 30;         // q = 2, 3
+    return make_float2(__uint_as_float(__float_as_uint(c0) ^ negc),
+                       __uint_as_float(__float_as_uint(s0) ^ negs));
+}
+
+// Box-Muller on the MUFU (lg2 / sqrt / sin / cos .approx); allowed only in the tf32 / bf16 modes,
+// whose operand rounding (2^-11 / 2^-8) dominates its error (reading R5: |fast - exact| <=
+// 2^-18 max(|z|, 1), checked exhaustively over every u1 and every u2 by tests/test_gpu_parity.py).
 __device__ __forceinline__ float2 box_muller_fast(uint32_t w1, uint32_t w2) {
     const uint32_t m = w1 >> 8;
     const float u1 = __uint2float_rn(m + 1u) * 0x1p-24f;
     const float v = __uint2float_rn(0xFFFFFFu - m) * 0x1p-24f;    // 1 - u1, exact
-    int32_t a = static_cast<int32_t>(w2 >> 8);
-    a = (a >= (1 << 23)) ? a - (1 << 24) : a;                      // u2 - round(u2), exact
-    const float th = __int2float_rn(a) * (6.28318530717958647692f * 0x1p-24f);
-    float lg, R, s, c;
+    float lg, R;
     asm("lg2.approx.f32 %0, %1;" : "=f"(lg) : "f"(u1));
     // lg2.approx has ~2^-22 ABSOLUTE error, which dominates -ln u1 when u1 -> 1; there use the
     // series -ln(1 - v) = v + v^2/2 + v^3/3 + v^4/4 (truncation < v^5/5 relative, v < 2^-5).
     const float series = v * fmaf(v, fmaf(v, fmaf(v, 0.25f, 0.333333343f), 0.5f), 1.0f);
     const float mln = (v < 0.03125f) ? series : lg * -0.693147180559945309f;  // -ln u1
     asm("sqrt.approx.f32 %0, %1;" : "=f"(R) : "f"(mln + mln));
-    asm("sin.approx.f32 %0, %1;" : "=f"(s) : "f"(th));
-    asm("cos.approx.f32 %0, %1;" : "=f"(c) : "f"(th));
-    return make_float2(R * c, R * s);
+    const float2 cs = cos_sin_2pi_fast(w2 >> 8);
+    return make_float2(R * cs.x, R * cs.y);
 }
 
 template <bool kFast>

@@ -147,6 +147,38 @@ cudaError_t launch_sum_peers(const float* const* src, int32_t n, int64_t elems, 
     return cudaGetLastError();
 }
 
+// Column-block pack (Redist All-to-All): out[rows * cb[j] + i * (cb[j+1] - cb[j]) + (c - cb[j])] =
+// B[i, c] for c in [cb[j], cb[j+1]).  One thread per element of B, reads coalesced along c.
+struct ColBounds {
+    int64_t b[65];
+    int32_t n;
+};
+__global__ void pack_cols_kernel(const float* __restrict__ B, int64_t rows, int64_t ldb, ColBounds cb,
+                                 float* __restrict__ out) {
+    const int64_t w = cb.b[cb.n];
+    const int64_t total = rows * w;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / w, c = idx - i * w;
+        int j = 0;
+        while (c >= cb.b[j + 1]) ++j;
+        const int64_t wj = cb.b[j + 1] - cb.b[j];
+        out[rows * cb.b[j] + i * wj + (c - cb.b[j])] = B[i * ldb + c];
+    }
+}
+
+cudaError_t launch_pack_cols(const float* B, int64_t rows, int64_t ldb, const int64_t* cb, int32_t nblk,
+                             float* out, cudaStream_t s) {
+    ColBounds c{};
+    for (int j = 0; j <= nblk; ++j) c.b[j] = cb[j];
+    c.n = nblk;
+    const int64_t total = rows * cb[nblk];
+    if (total <= 0) return cudaSuccess;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    pack_cols_kernel<<<blocks, 256, 0, s>>>(B, rows, ldb, c, out);
+    return cudaGetLastError();
+}
+
 // C[a, b] = sum_{c < chunks} part[c][a][b], r x nb, fixed order.
 __global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r, int32_t nb,
                                    float* __restrict__ C, int64_t ldc) {

@@ -17,20 +17,30 @@ Implements Alg. 1 (RandMatMul) and the No-Redist variant of Al
 
 Redist variant (Case 1 of the first grid-selection approach, p1 = q3 = P,
 PAPER.md:665-687, 698): B is computed row-block (zero communication), redistributed by an All-to-All
-so that rank k owns column block k of B over all n rows (bandwidth ~ n r / P words, PAPER.md:675;
-the pack / unpack of the paper's column-major exchange, is a strided copy here), and
-rank k computes the column block C[:, cols_k] = Omega^T B[:, cols_k] with Omega regenerated for all n
-rows.  The paper leaves C distributed; `nystrom_core_redist` all-gathers the column blocks so both
-variants return the same replicated C.
+so that rank k owns column block k of B over all n rows (bandwidth ~ n r / P words),
+and rank k computes the column block C[:, cols_k] = Omega^T B[:, cols_k] with Omega regenerated for
+all n rows.  The pack of the paper's exchange is the library's `sketch_pack_cols`
+kernel; no unpack is needed because the row-major blocks arrive in global row order.  The paper
+leaves C distributed; `nystrom_core_redist` all-gathers the column blocks so both variants return
+the same replicated C.
 
 Bandwidth accounting: predicted words per rank = (1 - 1/p2) n1 r / p1 for B (Alg. 1 cost,
 PAPER.md:427 with p3 = 1) plus the AllReduce payload r^2 for C; measured = bytes handed to
 the collectives.  Row splits are balanced; column splits are multiples of 128 (so each block's
 Omega rows start on a Philox row-group boundary) except the last.
+
+Communication goes through a `comm` object: `TorchComm` (torch.distributed process group + torch
+symmetric memory over NVLink) in production, or `VirtualComm` -- P virtual ranks as threads of ONE
+process on ONE device (SURVEY §4.2 "fake backend"): every rank's block runs through the same library
+calls, symmetric buffers are plain same-device allocations, and the reductions are the library's own
+fixed-order kernels (`sketch_sum_peers`, `sketch_reduce_slots`).  Nothing waits on the device for
+another rank's kernel in the virtual mode (the barrier is host-side, after a stream sync).
 """
 from __future__ import annotations
 
 import os
+import sys
+import threading
 
 from dataclasses import dataclass
 
@@ -85,21 +95,209 @@ def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool, var
     return int(round(4 * words))
 
 
-class DistSketch:
-    """B = A Omega and (optionally) C = Omega^T B on a p1 x p2 grid of ranks.
+# ============================================================================== communicators
+class SymmBuf:
+    """A buffer every rank of a group allocated together: `tensor` is this rank's, `ptrs[j]` the
+    device address of rank j's (NVLink peer mappings, or same-device addresses for virtual ranks);
+    `barrier()` orders every rank's prior writes before any rank's later reads."""
 
-    `local` is the per-rank compute: by default the CUDA library (paper_2603_20966_b200.Sketch);
-    tests may inject a CPU stand-in to exercise partitioning and collectives with gloo.
-    """
+    def __init__(self, tensor, ptrs, barrier, multicast_ptr: int = 0):
+        self.tensor, self.ptrs, self._barrier, self.multicast_ptr = tensor, list(ptrs), barrier, multicast_ptr
 
-    def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
-                 mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128,
-                 fused_rs=False, fused_ar: bool = False):
+    def barrier(self):
+        self._barrier()
+
+
+class TorchComm:
+    """torch.distributed process group; symmetric buffers from torch symmetric memory (NVLink)."""
+
+    def __init__(self, group=None):
         import torch.distributed as tdist
         self.tdist = tdist
         self.group = group
         self.rank = tdist.get_rank(group)
         self.world = tdist.get_world_size(group)
+
+    def split(self, groups: list) -> "TorchComm":
+        """Sub-communicator: `groups` lists the global ranks of every subgroup (all ranks call this with
+        the same list); returns the one this rank belongs to."""
+        me = self.tdist.get_rank()
+        mine = None
+        for g in groups:
+            pg = self.tdist.new_group(g)
+            if me in g:
+                mine = pg
+        return TorchComm(mine)
+
+    def reduce_scatter(self, out, inp):
+        self.tdist.reduce_scatter_tensor(out, inp, group=self.group)
+
+    def all_reduce(self, t, op: str = "sum"):
+        rop = {"sum": self.tdist.ReduceOp.SUM, "max": self.tdist.ReduceOp.MAX,
+               "min": self.tdist.ReduceOp.MIN}[op]
+        self.tdist.all_reduce(t, op=rop, group=self.group)
+
+    def all_to_all(self, recv, send, out_splits, in_splits):
+        self.tdist.all_to_all_single(recv, send, out_splits, in_splits, group=self.group)
+
+    def all_gather(self, out, inp):
+        self.tdist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def agree(self, ok: bool, device=None) -> bool:
+        """Collective: True iff `ok` on every rank (so a fallback is taken by all ranks or none)."""
+        import torch
+        backend = self.tdist.get_backend(self.group)
+        dev = device if (backend == "nccl" and device is not None) else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.tdist.all_reduce(t, op=self.tdist.ReduceOp.MIN, group=self.group)
+        return bool(int(t.item()))
+
+    def symmetric(self, shape, dtype, device) -> SymmBuf:
+        """Raises if symmetric memory cannot be set up here (the caller decides collectively)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        grp = self.group if self.group is not None else self.tdist.group.WORLD
+        buf = symm_mem.empty(shape, dtype=dtype, device=device)
+        hdl = symm_mem.rendezvous(buf, grp.group_name)
+        mc = 0
+        try:
+            if hdl.has_multicast_support():
+                mc = int(hdl.multicast_ptr)
+        except Exception:  # pragma: no cover - older torch
+            mc = 0
+        return SymmBuf(buf, [int(x) for x in hdl.buffer_ptrs], lambda: hdl.barrier(channel=0), mc)
+
+
+class VirtualWorld:
+    """Shared state of P virtual ranks (threads of one process on one device)."""
+
+    def __init__(self, world: int, timeout: float = 300.0):
+        self.world = world
+        self.timeout = timeout
+        self._lock = threading.Lock()
+        self._groups = {}  # members tuple -> (threading.Barrier, board dict)
+
+    def group(self, members: tuple):
+        with self._lock:
+            g = self._groups.get(members)
+            if g is None:
+                g = (threading.Barrier(len(members), timeout=self.timeout), {})
+                self._groups[members] = g
+            return g
+
+
+class VirtualComm:
+    """One virtual rank of a `VirtualWorld` (SURVEY §4.2 single-GPU "virtual ranks" backend).
+
+    Collectives: every member deposits its tensor after synchronising its own stream, a host barrier,
+    then each member computes its result from the others' device buffers -- reductions with the
+    library's fixed-order `sketch_sum_peers` kernel (rank order), data movement with device copies."""
+
+    def __init__(self, vw: VirtualWorld, rank: int, members=None):
+        self.vw = vw
+        self.members = tuple(members) if members is not None else tuple(range(vw.world))
+        self.grank = rank
+        self.rank = self.members.index(rank)
+        self.world = len(self.members)
+        self._bar, self._board = vw.group(self.members)
+        self._seq = 0
+
+    def split(self, groups: list) -> "VirtualComm":
+        for g in groups:
+            if self.grank in g:
+                return VirtualComm(self.vw, self.grank, g)
+        raise ValueError("rank in no subgroup")
+
+    @staticmethod
+    def _sync():
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.current_stream().synchronize()
+
+    def _exchange(self, obj):
+        """All members' `obj`, in rank order (host-side rendezvous after a stream sync)."""
+        self._sync()
+        key = self._seq
+        self._seq += 1
+        self._board[(key, self.rank)] = obj
+        self._bar.wait()
+        objs = [self._board[(key, j)] for j in range(self.world)]
+        self._bar.wait()  # everyone has read: the slot may be dropped
+        self._board.pop((key, self.rank), None)
+        return objs
+
+    def _sum_into(self, out, srcs):
+        """out = srcs[0] + srcs[1] + ... (rank order) with the library's sum_peers kernel."""
+        import torch
+        if out.is_cuda and out.numel() % 4 == 0 and all(s.data_ptr() % 16 == 0 for s in srcs) \
+                and out.data_ptr() % 16 == 0 and all(s.is_contiguous() for s in srcs) and out.is_contiguous():
+            from . import sum_peers
+            sum_peers([s.data_ptr() for s in srcs], out.numel(), out)
+        else:
+            acc = srcs[0].clone()
+            for s in srcs[1:]:
+                acc += s
+            out.copy_(acc.view_as(out))
+
+    def reduce_scatter(self, out, inp):
+        ins = self._exchange(inp)
+        n = out.numel()
+        self._sum_into(out.view(-1), [t.reshape(-1)[self.rank * n:(self.rank + 1) * n] for t in ins])
+        self._exchange(None)  # inputs may be reused after every member has read them
+
+    def all_reduce(self, t, op: str = "sum"):
+        ins = self._exchange(t.clone())
+        if op == "sum":
+            self._sum_into(t.view(-1), [x.reshape(-1) for x in ins])
+        else:
+            import torch
+            acc = ins[0].clone()
+            for x in ins[1:]:
+                acc = torch.maximum(acc, x) if op == "max" else torch.minimum(acc, x)
+            t.copy_(acc)
+
+    def all_to_all(self, recv, send, out_splits, in_splits):
+        ins = self._exchange((send, list(in_splits)))
+        off = 0
+        for j, (s, splits) in enumerate(ins):
+            a = sum(splits[:self.rank])
+            n = splits[self.rank]
+            assert n == out_splits[j]
+            recv[off:off + n].copy_(s[a:a + n])
+            off += n
+        self._exchange(None)
+
+    def all_gather(self, out, inp):
+        ins = self._exchange(inp)
+        n = inp.numel()
+        for j, x in enumerate(ins):
+            out.view(-1)[j * n:(j + 1) * n].copy_(x.reshape(-1))
+        self._exchange(None)
+
+    def agree(self, ok: bool, device=None) -> bool:
+        return all(self._exchange(bool(ok)))
+
+    def symmetric(self, shape, dtype, device) -> SymmBuf:
+        import torch
+        buf = torch.empty(shape, dtype=dtype, device=device)
+        ptrs = self._exchange(buf.data_ptr())
+        return SymmBuf(buf, ptrs, lambda: self._exchange(None))
+
+
+# ============================================================================== the layouts
+class DistSketch:
+    """B = A Omega and (optionally) C = Omega^T B on a p1 x p2 grid of ranks.
+
+    `local` is the per-rank compute: by default the CUDA library (paper_2603_20966_b200.Sketch);
+    CPU tests may inject an oracle stand-in to exercise partitioning and collectives with gloo.
+    `comm` defaults to a TorchComm over `group`.
+    """
+
+    def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
+                 mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128,
+                 fused_rs=False, fused_ar: bool = False, comm=None):
+        self.comm = comm if comm is not None else TorchComm(group)
+        self.rank = self.comm.rank
+        self.world = self.comm.world
         if layout.P != self.world:
             raise ValueError("layout size != world size")
         self.layout = layout
@@ -112,20 +310,15 @@ class DistSketch:
             local = Sketch(seed, dist, n2, r, mode=mode, omega=omega)
         self.local = local
         # row group {(i, *)} for the reduce-scatter of B
-        self.row_group = group
+        self.row_comm = self.comm
         if layout.p2 > 1 and layout.p1 > 1:
-            groups = [tdist.new_group([ii * layout.p2 + jj for jj in range(layout.p2)])
-                      for ii in range(layout.p1)]
-            self.row_group = groups[self.i]
-        elif layout.p2 > 1:
-            self.row_group = group
+            self.row_comm = self.comm.split([[ii * layout.p2 + jj for jj in range(layout.p2)]
+                                             for ii in range(layout.p1)])
         self.comm_bytes = 0
-        # f1: reduce-scatter of partial B fused into the GEMM epilogue (NVLink stores into the owners'
-        # symmetric-memory receive buffers) instead of an NCCL reduce_scatter after the GEMM
-        # reduce-scatter of partial B for p2 > 1: False / "nccl" = NCCL reduce_scatter; "peer" = B-bar
-        # written into a symmetric-memory slot, one device barrier, each owner sums its piece from
-        # the p2 slots over NVLink in rank order; True / "epilogue" = the GEMM epilogue stores
-        # straight into the owners' slots
+        # reduce-scatter of partial B for p2 > 1: False / "nccl" = NCCL reduce_scatter;
+        # "peer" = B-bar written into a symmetric-memory slot, one device barrier, each owner sums its
+        # piece from the p2 slots over NVLink in rank order; True / "epilogue" = the GEMM epilogue
+        # stores straight into the owners' slots
         mode = {False: "nccl", None: "nccl", True: "epilogue"}.get(fused_rs, fused_rs)
         if mode not in ("nccl", "peer", "epilogue"):
             raise ValueError(f"unknown reduce-scatter mode {fused_rs!r}")
@@ -136,8 +329,26 @@ class DistSketch:
         self._rs = None
         self._rsp = None
         # f1: the AllReduce of C as one NVLink peer-read sum instead of NCCL (symmetric memory)
-        self.fused_ar = bool(fused_ar)
+        self.fused_ar = bool(fused_ar) and r % 4 == 0
         self._ar = None
+        self.fallbacks = []  # (what, error) of symmetric-memory setups that fell back to NCCL
+
+    # ------------------------------------------------------------------ symmetric memory setup
+    def _symm(self, comm, shape, device, what):
+        """Allocate + rendezvous a symmetric buffer on `comm`; the decision to fall back to NCCL is
+        collective (all ranks of `comm` agree), so no rank is left waiting in a barrier.  Only the
+        setup is guarded: failures of the compute calls propagate."""
+        import torch
+        buf, err = None, None
+        try:
+            buf = comm.symmetric(shape, torch.float32, device)
+        except Exception as e:  # symmetric memory unavailable on this box
+            err = e
+        if comm.agree(buf is not None, device):
+            return buf
+        self.fallbacks.append((what, repr(err)))
+        print(f"[dist] {what} over symmetric memory unavailable ({err!r}); using NCCL", file=sys.stderr)
+        return None
 
     # ------------------------------------------------------------------ partition
     def a_block_range(self) -> tuple:
@@ -166,56 +377,47 @@ class DistSketch:
         rows = r1 - r0
         per = -(-rows // p2)
         if self.rs_mode == "epilogue":
-            return self._apply_fused_rs(A_blk, rows, per, c0)
+            out = self._apply_fused_rs(A_blk, rows, per, c0)
+            if out is not None:
+                return out
         if self.rs_mode == "peer":
-            try:
-                return self._apply_peer_rs(A_blk, rows, per, c0)
-            except Exception as e:  # symmetric memory unavailable: NCCL from now on (same results)
-                self._fallback("peer-read reduce-scatter", e)
+            out = self._apply_peer_rs(A_blk, rows, per, c0)
+            if out is not None:
+                return out
         Bbar = torch.zeros((per * p2, self.r), dtype=torch.float32, device=A_blk.device)
         self.local.apply_block(A_blk, c0, out=Bbar[:rows])
         piece = torch.empty((per, self.r), dtype=torch.float32, device=A_blk.device)
-        self.tdist.reduce_scatter_tensor(piece, Bbar, group=self.row_group)
+        self.row_comm.reduce_scatter(piece, Bbar)
         self.comm_bytes += Bbar.numel() * 4 * (p2 - 1) // p2
         a, b = self.b_piece_rows()
         return piece[: b - a], (a, b)
 
-    def _fallback(self, what, err):
-        """Symmetric memory could not be set up (every rank hits the same condition): use NCCL."""
-        import sys
-        print(f"[dist] {what} over symmetric memory unavailable ({err!r}); using NCCL", file=sys.stderr)
-        if self.rs_mode in ("peer", "epilogue"):
-            self.rs_mode, self.fused_rs = "nccl", False
-        self.fused_ar = False
-
     def _apply_peer_rs(self, A_blk, rows, per, c0):
         """Alg. 1 line 415 over symmetric memory: B-bar (rows padded to p2 * per) is written into this
         rank's slot (two slots alternating per call), one device barrier over the row group, then the
-        owner of piece j sums rows [j per, (j+1) per) of the p2 slots over NVLink in rank order."""
+        owner of piece j sums rows [j per, (j+1) per) of the p2 slots over NVLink in rank order.
+        Returns None (and switches to NCCL on every rank) if symmetric memory cannot be set up."""
         import torch
         from . import sum_peers
         p2, r = self.layout.p2, self.r
         key = (rows, per)
         if self._rsp is None or self._rsp["key"] != key:
-            import torch.distributed._symmetric_memory as symm_mem
-            grp = self.row_group if self.row_group is not None else self.tdist.group.WORLD
-            try:
-                symm_mem.enable_symm_mem_for_group(grp.group_name)
-            except Exception:  # pragma: no cover
-                pass
-            buf = symm_mem.empty((2, p2 * per, r), dtype=torch.float32, device=A_blk.device)
-            buf.zero_()  # padding rows of the last piece stay zero
-            hdl = symm_mem.rendezvous(buf, grp.group_name)
-            self._rsp = {"key": key, "buf": buf, "hdl": hdl, "ptrs": [int(x) for x in hdl.buffer_ptrs], "k": 0}
+            sb = self._symm(self.row_comm, (2, p2 * per, r), A_blk.device, "peer-read reduce-scatter")
+            if sb is None:
+                self.rs_mode, self.fused_rs = "nccl", False
+                return None
+            sb.tensor.zero_()  # padding rows of the last piece stay zero
+            self._rsp = {"key": key, "sb": sb, "k": 0}
         st = self._rsp
         k = st["k"]
         st["k"] ^= 1
-        self.local.apply_block(A_blk, c0, out=st["buf"][k][:rows])
-        st["hdl"].barrier(channel=0)  # every rank's B-bar is in its slot k
+        sb = st["sb"]
+        self.local.apply_block(A_blk, c0, out=sb.tensor[k][:rows])
+        sb.barrier()  # every rank's B-bar is in its slot k
         a, b = self.b_piece_rows()
         piece = torch.empty((per, r), dtype=torch.float32, device=A_blk.device)
         off = (k * p2 * per + self.j * per) * r * 4
-        sum_peers([p + off for p in st["ptrs"]], per * r, piece)
+        sum_peers([p + off for p in sb.ptrs], per * r, piece)
         self.comm_bytes += 4 * per * r * (p2 - 1)
         return piece[: b - a], (a, b)
 
@@ -228,31 +430,26 @@ class DistSketch:
         npad = -(-self.r // 16) * 16
         k = A_blk.shape[1]
         if self._rs is None or self._rs["key"] != (rows, per, k):
-            import torch.distributed._symmetric_memory as symm_mem
-            grp = self.row_group if self.row_group is not None else self.tdist.group.WORLD
             # split-K partials would each cross NVLink (S x the reduce-scatter bytes): default to no
-            # split; RS_SPLIT=auto takes the local plan's choice (max over the row group)
+            # split; SK_RS_SPLIT=auto takes the local plan's choice (max over the row group)
             if os.environ.get("SK_RS_SPLIT", "1") == "auto":
                 split = torch.tensor([self.local.rs_split(rows, k)], dtype=torch.int32, device=A_blk.device)
-                self.tdist.all_reduce(split, op=self.tdist.ReduceOp.MAX, group=grp)  # same slot layout everywhere
+                self.row_comm.all_reduce(split, op="max")  # same slot layout everywhere
                 split = int(split.item())
             else:
                 split = max(1, int(os.environ.get("SK_RS_SPLIT", "1")))
-            try:
-                symm_mem.enable_symm_mem_for_group(grp.group_name)
-            except Exception:  # pragma: no cover - newer torch enables it implicitly
-                pass
-            buf = symm_mem.empty((p2 * split * per * npad,), dtype=torch.float32, device=A_blk.device)
-            hdl = symm_mem.rendezvous(buf, grp.group_name)
-            ptrs = [int(hdl.buffer_ptrs[j]) for j in range(p2)]
-            self._rs = {"key": (rows, per, k), "buf": buf, "hdl": hdl, "ptrs": ptrs, "split": split, "npad": npad}
+            sb = self._symm(self.row_comm, (p2 * split * per * npad,), A_blk.device, "epilogue reduce-scatter")
+            if sb is None:
+                self.rs_mode, self.fused_rs = "nccl", False
+                return None
+            self._rs = {"key": (rows, per, k), "sb": sb, "split": split, "npad": npad}
         rs = self._rs
-        hdl, split = rs["hdl"], rs["split"]
-        hdl.barrier(channel=0)  # the owners have consumed the previous step's slots
-        self.local.apply_block_rs(A_blk, c0, rs["ptrs"], per, self.j, per * npad, split)
-        hdl.barrier(channel=0)  # every rank's stores have landed
+        sb, split = rs["sb"], rs["split"]
+        sb.barrier()  # the owners have consumed the previous step's slots
+        self.local.apply_block_rs(A_blk, c0, sb.ptrs[:p2], per, self.j, per * npad, split)
+        sb.barrier()  # every rank's stores have landed
         a, b = self.b_piece_rows()
-        piece = self.local.reduce_slots(rs["buf"], p2 * split, per * npad, b - a)
+        piece = self.local.reduce_slots(sb.tensor, p2 * split, per * npad, b - a)
         # bytes this rank stored into other ranks' slots (split partials, rows padded to npad)
         mine = [min(rows, (jj + 1) * per) - min(rows, jj * per) for jj in range(p2)]
         self.comm_bytes += 4 * split * npad * (rows - mine[self.j])
@@ -272,20 +469,21 @@ class DistSketch:
         k = self.rank
         nbk = cb[k + 1] - cb[k]
         rows = [self.row_bnd[j + 1] - self.row_bnd[j] for j in range(P)]
-        send = torch.cat([Bp[:, cb[j]:cb[j + 1]].reshape(-1) for j in range(P)])  # pack by column block
+        # pack by column block: block j = B[:, cb[j]:cb[j+1]] row-major, contiguous
+        send = self.local.pack_cols(Bp, cb)
         in_splits = [(b - a) * (cb[j + 1] - cb[j]) for j in range(P)]
         out_splits = [rows[j] * nbk for j in range(P)]
         recv = torch.empty(sum(out_splits), dtype=torch.float32, device=Bp.device)
-        self.tdist.all_to_all_single(recv, send, out_splits, in_splits, group=self.group)
+        self.comm.all_to_all(recv, send, out_splits, in_splits)
         self.comm_bytes += 4 * (sum(in_splits) - in_splits[k])
-        Bcol = recv.view(self.n1, nbk)  # rows arrive in rank order = global row order
-        Ccol = self.local.core_block_cols(Bcol, 0)  # r x nbk, Omega regenerated for all n rows
-        # replicate C: all-gather the column blocks (padded to the largest block)
+        Bcol = recv.view(self.n1, nbk)  # rows arrive in rank order = global row order: no unpack
         width = max(cb[j + 1] - cb[j] for j in range(P))
+        # column block of C = Omega^T B[:, cols_k], Omega regenerated for all n rows, written into a
+        # block padded to the widest column block for the all-gather that replicates C
         pad = torch.zeros((r, width), dtype=torch.float32, device=Bp.device)
-        pad[:, :nbk] = Ccol
+        self.local.core_block_cols(Bcol, 0, out=pad[:, :nbk])
         gathered = torch.empty(P * r * width, dtype=torch.float32, device=Bp.device)
-        self.tdist.all_gather_into_tensor(gathered, pad.reshape(-1), group=self.group)
+        self.comm.all_gather(gathered, pad.reshape(-1))
         gathered = gathered.view(P, r, width)
         self.comm_bytes += 4 * r * width * (P - 1)
         C = torch.cat([gathered[j, :, : cb[j + 1] - cb[j]] for j in range(P)], dim=1)
@@ -296,13 +494,12 @@ class DistSketch:
         """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank."""
         Bp, (a, b) = self.apply(A_blk)
         if self.world > 1 and self.fused_ar:
-            try:
-                return Bp, (a, b), self._core_fused_allreduce(Bp, a)
-            except Exception as e:  # symmetric memory unavailable: NCCL from now on (same results)
-                self._fallback("fused AllReduce", e)
+            C = self._core_fused_allreduce(Bp, a)
+            if C is not None:
+                return Bp, (a, b), C
         C = self.local.core_block(Bp, a)
         if self.world > 1:
-            self.tdist.all_reduce(C, group=self.group)
+            self.comm.all_reduce(C)
             self.comm_bytes += C.numel() * 4
         return Bp, (a, b), C
 
@@ -314,21 +511,55 @@ class DistSketch:
         from . import sum_peers
         r = self.r
         if self._ar is None:
-            import torch.distributed._symmetric_memory as symm_mem
-            grp = self.group if self.group is not None else self.tdist.group.WORLD
-            try:
-                symm_mem.enable_symm_mem_for_group(grp.group_name)
-            except Exception:  # pragma: no cover
-                pass
-            buf = symm_mem.empty((2, r * r), dtype=torch.float32, device=Bp.device)
-            hdl = symm_mem.rendezvous(buf, grp.group_name)
-            self._ar = {"buf": buf, "hdl": hdl, "ptrs": [int(x) for x in hdl.buffer_ptrs], "k": 0}
+            sb = self._symm(self.comm, (2, r * r), Bp.device, "fused AllReduce")
+            if sb is None:
+                self.fused_ar = False
+                return None
+            self._ar = {"sb": sb, "k": 0}
         ar = self._ar
         k = ar["k"]
         ar["k"] ^= 1
-        self.local.core_block(Bp, a, out=ar["buf"][k].view(r, r))
-        ar["hdl"].barrier(channel=0)  # every rank's partial is in its slot k
+        sb = ar["sb"]
+        self.local.core_block(Bp, a, out=sb.tensor[k].view(r, r))
+        sb.barrier()  # every rank's partial is in its slot k
         C = torch.empty((r, r), dtype=torch.float32, device=Bp.device)
-        sum_peers([p + k * r * r * 4 for p in ar["ptrs"]], r * r, C)
+        sum_peers([p + k * r * r * 4 for p in sb.ptrs], r * r, C)
         self.comm_bytes += r * r * 4
         return C
+
+
+def run_virtual(world: int, fn, timeout: float = 600.0):
+    """Runs fn(comm) for `world` virtual ranks (threads, each on its own CUDA stream of the current
+    device when CUDA is available); returns the results in rank order, re-raising the first error."""
+    import torch
+    vw = VirtualWorld(world)
+    res, errs = [None] * world, [None] * world
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+
+    def body(rank):
+        try:
+            if dev is not None:
+                torch.cuda.set_device(dev)
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    res[rank] = fn(VirtualComm(vw, rank))
+                    s.synchronize()
+            else:
+                res[rank] = fn(VirtualComm(vw, rank))
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errs[rank] = e
+            for bar, _ in list(vw._groups.values()):
+                bar.abort()
+
+    ts = [threading.Thread(target=body, args=(i,)) for i in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+    for e in errs:
+        if e is not None and not isinstance(e, threading.BrokenBarrierError):
+            raise e
+    for e in errs:
+        if e is not None:
+            raise e
+    return res

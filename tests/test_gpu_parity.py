@@ -89,9 +89,41 @@ def test_box_muller_ulp_sweeps(transform):
         assert _ulp(go.cpu().numpy(), ro).max() <= 2
 
 
-def test_box_muller_fast_close():
-    """Fast (MUFU) transform: error <= 2^-16 * max(|z|, 1) on random pairs (reading R5: far below
-    the 2^-11 tf32 / 2^-8 bf16 operand rounding it is allowed under)."""
+def _fast_err(g, r):
+    return np.abs(np.asarray(g, np.float64) - r) / np.maximum(np.abs(r), 1.0)
+
+
+FAST_BOUND = 2.0 ** -18  # reading R5: |fast - exact| <= 2^-18 max(|z|, 1)
+
+
+def test_box_muller_fast_sweeps():
+    """Fast (MUFU) transform, exhaustively like the accurate one: every u1 (u2 = 0, so z_even = R and
+    z_odd must be exactly 0) and every u2 at four u1 values, against the correctly rounded oracle:
+    error <= 2^-18 max(|z|, 1) (reading R5), exact zeros at u2 in {0, 1/4, 1/2, 3/4} (reading R14)."""
+    sk = _sk()
+    n = 1 << 24
+    w1 = (np.arange(n, dtype=np.uint64) << 8).astype(np.uint32)
+    w2 = np.zeros(n, dtype=np.uint32)
+    ge, go = sk.debug_box_muller(_dev(w1.view(np.int32)), _dev(w2.view(np.int32)), "fast")
+    re_, ro = oracle.box_muller_many(w1, w2)
+    worst = _fast_err(ge.cpu().numpy(), re_).max()
+    assert np.all(go.cpu().numpy() == 0.0)
+    for u1 in (0, 12345, 1 << 23, (1 << 24) - 2):
+        w1c = np.full(n, u1 << 8, dtype=np.uint32)
+        ge, go = sk.debug_box_muller(_dev(w1c.view(np.int32)), _dev(w1.view(np.int32)), "fast")
+        re_, ro = oracle.box_muller_many(w1c, w1)
+        ge, go = ge.cpu().numpy(), go.cpu().numpy()
+        worst = max(worst, _fast_err(ge, re_).max(), _fast_err(go, ro).max())
+        # quarter turns: u2 = k/4 -> exactly one of cos / sin is zero
+        for k, (zc, zs) in enumerate(((False, True), (True, False), (False, True), (True, False))):
+            i = k << 22
+            assert (ge[i] == 0.0) == zc and (go[i] == 0.0) == zs, (u1, k, ge[i], go[i])
+    print(f"fast Box-Muller: max |fast - exact| / max(|z|,1) = 2^{np.log2(worst):.2f}")
+    assert worst <= FAST_BOUND
+
+
+def test_box_muller_fast_random_pairs():
+    """... and on 4M random (u1, u2) pairs."""
     sk = _sk()
     rng = np.random.default_rng(0)
     n = 1 << 22
@@ -100,8 +132,7 @@ def test_box_muller_fast_close():
     ge, go = sk.debug_box_muller(_dev(w1.view(np.int32)), _dev(w2.view(np.int32)), "fast")
     re_, ro = oracle.box_muller_many(w1, w2)
     for g, r in ((ge.cpu().numpy(), re_), (go.cpu().numpy(), ro)):
-        err = np.abs(g.astype(np.float64) - r) / np.maximum(np.abs(r), 1.0)
-        assert err.max() <= 2.0**-16
+        assert _fast_err(g, r).max() <= FAST_BOUND
 
 
 # ----------------------------------------------------------------------------- B = A Omega
