@@ -234,7 +234,7 @@ def run_reference(args, W, wl_name):
     sample = (f"{rows} of {W['n1']} rows of A per step (full K={W['n2']}, r={W['r']}); Omega "
               f"materialised in fp64 once per call" + ("; + Omega^T B of the sample rows" if W["nystrom"] else ""))
     line = {
-        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": max(world, args.gpus),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": W["desc"], "n1": W["n1"], "n2": W["n2"], "r": W["r"], "dist": W["dist"],
@@ -316,6 +316,20 @@ def omega_ablation(args, W, sk, local, A, ds, dev, world, rank, stream, barrier,
 
 
 # ----------------------------------------------------------------------------- our arm
+def relaunch_under_torchrun(n: int) -> None:
+    """Re-executes this command as `torch.distributed.run --nproc-per-node n` on 127.0.0.1 and exits
+    with its status (rank 0 prints the JSON line)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    log("[bench] launching " + " ".join(cmd[1:]))
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -355,6 +369,13 @@ def main():
     W = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args, W, args.workload)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        # `bench.py --gpus N` outside a launcher: start the N ranks (one process per GPU) ourselves
+        return relaunch_under_torchrun(args.gpus)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        log(f"[bench] --gpus {args.gpus} does not match WORLD_SIZE={ws_env}; refusing to run")
+        sys.exit(2)
     args.warmup = max(args.warmup, 3)
     if args.omega == "auto":
         args.omega = "fast" if args.mode == "bf16" else "accurate"
@@ -419,14 +440,17 @@ def main():
     sampler.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e0.record(stream)
     h0 = time.perf_counter()
-    for _ in range(args.steps):
+    for i in range(args.steps):
         out = step()
+        step_ev[i].record(stream)  # per-step boundaries (median); the total is e0 -> e1
     host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host submission time per step
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    per_step = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
     launches = sk.launch_count() - launches0
     phases = local.profile_read()
     local.set_profiling(False)
@@ -454,12 +478,15 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         h0 = time.perf_counter()
-        for _ in range(args.steps):
+        for i in range(args.steps):
             g.replay()
+            step_ev[i].record(stream)
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         e1.record(stream)
         torch.cuda.synchronize()
         t_ms = e0.elapsed_time(e1)
+        per_step = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i])
+                                                    for i in range(1, args.steps)]
         launches = launches_per_step * args.steps
         graph_info = {"replayed": True, "launches_per_step": launches_per_step,
                       "eager_ms_per_step": eager_ms_step}
@@ -470,6 +497,10 @@ def main():
         tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
     t_ms = float(tmax.item())
     ms_step = t_ms / args.steps
+    med = torch.tensor([statistics.median(per_step)], dtype=torch.float64, device=dev if world > 1 else "cpu")
+    if world > 1:
+        tdist.all_reduce(med, op=tdist.ReduceOp.MAX)
+    ms_step_median = float(med.item())
     a_bytes_total = 4.0 * n1 * n2
     value = a_bytes_total / (ms_step * 1e-3) / 1e9
     flops = 2.0 * n1 * n2 * r + (2.0 * n2 * r * r if W["nystrom"] else 0.0)
@@ -511,7 +542,8 @@ def main():
 
     result = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_median": ms_step_median,
+        "value_median": a_bytes_total / (ms_step_median * 1e-3) / 1e9, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": args.mode, "data": "synthetic (seeded, generated in HBM)",
         "config": {"workload": W["desc"], "n1": n1, "n2": n2, "r": r, "dist": W["dist"], "mode": args.mode,
                    "omega_transform": args.omega, "layout": f"{layout.p1}x{layout.p2}",

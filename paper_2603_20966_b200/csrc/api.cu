@@ -258,6 +258,9 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     }
     if (best_s > 1 && force_split == 0 && ws_cap < static_cast<size_t>(best_s) * P.ws_per_split)
         best_s = std::max<int>(1, static_cast<int>(ws_cap / P.ws_per_split));
+    // tf32x3's accuracy cap holds whatever asked for the split (override, fused reduce-scatter, a
+    // short workspace: the caller's workspace_size covers min_split partials)
+    best_s = std::max(best_s, std::min(min_split, std::max(1, P.kiters)));
     // each split must own >= 1 K iteration
     const int kper = (P.kiters + best_s - 1) / best_s;
     P.split = (P.kiters + kper - 1) / kper;
@@ -374,7 +377,8 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
     const int roff = static_cast<int>(k0 & 3);
     const SketchPlan P = plan_sketch(h, m, k, kshift, rs ? ~size_t(0) : ws_bytes, rs ? rs->split : 0);
     if (rs && (P.npass != 1 || P.split != rs->split))
-        return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256 and split <= K iterations");
+        return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256, split <= K iterations and, in "
+                                        "tf32x3, split >= sketch_rs_split (K per accumulator <= 1024)");
     CUtensorMap map;
     sk_status_t st = make_map_2d(&map, A, m, k, lda, 32, 128);
     if (st != SK_SUCCESS) return st;
@@ -522,13 +526,12 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
 
 namespace sk {
 int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
+    static const int n = [] {  // thread-safe one-time initialisation
+        int dev = 0, v = 0;
         cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-            n = 148;
-    }
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        return v;
+    }();
     return n;
 }
 }  // namespace sk

@@ -324,12 +324,7 @@ static cudaError_t launch_core_tc_one(const CUtensorMap& tmB, const CUtensorMap&
                                       cudaStream_t s) {
     auto kern = core_gemm_tc_kernel<NACC, DIST, MODE, FAST>;
     const size_t smem = core_gemm_tc_smem_bytes(NACC, p.npad);
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        smem_set = smem;
-    }
+    if (cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(kern), smem)) return e;
     const dim3 grid(p.nchunks, (p.r + 255) / 256, (p.nb + 255) / 256);
     kern<<<grid, kCoreThreads, smem, s>>>(tmB, tmOut, p);
     return cudaGetLastError();

@@ -96,6 +96,7 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa,
                               bool olo, int ks, int nsubo, int y_stages);
 int sketch_gemm_max_smem();
+cudaError_t raise_smem_limit(const void* fn, size_t smem);
 
 cudaError_t launch_pack_cols(const float* B, int64_t rows, int64_t ldb, const int64_t* cb, int32_t nblk,
                              float* out, cudaStream_t s);

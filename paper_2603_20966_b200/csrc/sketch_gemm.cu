@@ -18,6 +18,10 @@
 //               Warps 4-7 also run the epilogue (tcgen05.ld 32x32b -> st.global of B or of a
 //               split-K partial).
 // Work unit = (m-block of 128*CG*NACC rows, K split s); units are dealt round-robin to CTA groups.
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "kernels.cuh"
 #include "omega_tile.cuh"
 #include "philox.cuh"
@@ -659,6 +663,21 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     }
 }
 
+// Raises a kernel's opt-in dynamic smem limit to at least `smem` (per device and function; thread-safe,
+// the attribute only ever grows).
+cudaError_t raise_smem_limit(const void* fn, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> set;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = set[std::make_pair(dev, fn)];
+    if (smem <= cur) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e == cudaSuccess) cur = smem;
+    return e;
+}
+
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa, bool olo,
                               int ks, int nsubo, int y_stages) {
     return make_layout(nacc, npad / cg, a_stages, o_stages, xa, olo, ks, nsubo, y_stages).total + 1024;
@@ -669,9 +688,18 @@ int sketch_gemm_max_smem() { return 227 * 1024; }
 // Clusters of `cluster` CTAs of this kernel that can be co-resident (GPC packing strands SMs for
 // clusters of 4).  Returns 0 if the query fails.
 int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem) {
-    static int cache[5][4][2] = {};  // [cl][mode][fast] + 1, per process
-    const int ci = cl >= 1 && cl <= 4 ? cl : 0;
-    if (mode >= 0 && mode < 4 && cache[ci][mode][fast ? 1 : 0] > 0) return cache[ci][mode][fast ? 1 : 0] - 1;
+    // per process, keyed by (device, kernel instantiation, smem); guarded: handles may be used from
+    // several threads at once (sketch.h)
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int, int, int, int, size_t>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, cg, nacc, dist, mode, fast ? 1 : 0, cl, smem);
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cg * cl * 64);
     cfg.blockDim = dim3(threads_for(mode));
@@ -701,10 +729,10 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
     }
 #undef SK_FN
     if (!fn) return 0;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
-        return 0;
+    if (raise_smem_limit(fn, smem) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) return 0;
-    if (mode >= 0 && mode < 4) cache[ci][mode][fast ? 1 : 0] = n + 1;
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = n;
     return n;
 }
 
@@ -712,13 +740,7 @@ template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL>
 static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p, int grid,
                               size_t smem, cudaStream_t s) {
     auto kern = sketch_gemm_kernel<CG, NACC, DIST, MODE, FAST, CL>;
-    static size_t smem_set = 0;  // per instantiation: raise the opt-in smem limit once
-    if (smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        smem_set = smem;
-    }
+    if (cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(kern), smem)) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(threads_for(MODE));

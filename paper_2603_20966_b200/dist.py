@@ -254,6 +254,7 @@ class VirtualComm:
             for x in ins[1:]:
                 acc = torch.maximum(acc, x) if op == "max" else torch.minimum(acc, x)
             t.copy_(acc)
+        self._exchange(None)  # every member's reads of the others' copies are done (stream-synced)
 
     def all_to_all(self, recv, send, out_splits, in_splits):
         ins = self._exchange((send, list(in_splits)))
@@ -432,12 +433,14 @@ class DistSketch:
         if self._rs is None or self._rs["key"] != (rows, per, k):
             # split-K partials would each cross NVLink (S x the reduce-scatter bytes): default to no
             # split; SK_RS_SPLIT=auto takes the local plan's choice (max over the row group)
-            if os.environ.get("SK_RS_SPLIT", "1") == "auto":
-                split = torch.tensor([self.local.rs_split(rows, k)], dtype=torch.int32, device=A_blk.device)
-                self.row_comm.all_reduce(split, op="max")  # same slot layout everywhere
-                split = int(split.item())
-            else:
-                split = max(1, int(os.environ.get("SK_RS_SPLIT", "1")))
+            # tf32x3 caps K per TMEM accumulator: at least the local plan's split there
+            x3 = getattr(self.local, "mode", None) == "tf32x3"
+            env = os.environ.get("SK_RS_SPLIT", "1")
+            split = 1 if env == "auto" else max(1, int(env))
+            if env == "auto" or x3:
+                t = torch.tensor([max(split, self.local.rs_split(rows, k))], dtype=torch.int32, device=A_blk.device)
+                self.row_comm.all_reduce(t, op="max")  # same slot layout everywhere
+                split = int(t.item())
             sb = self._symm(self.row_comm, (p2 * split * per * npad,), A_blk.device, "epilogue reduce-scatter")
             if sb is None:
                 self.rs_mode, self.fused_rs = "nccl", False

@@ -153,3 +153,30 @@ def test_redist_variant_matches_noredist(world):
         assert np.array_equal(C.astype(np.float64), Cref)
         pred = predicted_bytes_per_rank(n, r, Layout(world, 1), True, "redist")
         assert comm == pred
+
+
+@pytest.mark.parametrize("world,spec,variant", [(2, "col", "noredist"), (4, "2x2", "noredist"),
+                                                (8, "4x2", "noredist"), (4, "row", "redist")])
+def test_virtual_comm_matches_oracle(world, spec, variant):
+    """The single-process virtual-rank backend (VirtualComm) on CPU: same exact B pieces and
+    C as the oracle of the whole problem, and the same byte accounting as the gloo process groups."""
+    from paper_2603_20966_b200.dist import run_virtual
+    n, r = 520, 24
+    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+    Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
+    layout = Layout.parse(spec, world)
+
+    def body(comm):
+        ds = DistSketch(SEED, "rademacher", n, n, r, layout, local=OracleLocal(SEED, "rademacher", r), comm=comm)
+        r0, r1, c0, c1 = ds.a_block_range()
+        Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1]))
+        Bp, (a, b), C = ds.nystrom_core_redist(Ablk) if variant == "redist" else ds.nystrom_core(Ablk)
+        return a, b, Bp.numpy(), C.numpy(), ds.comm_bytes
+
+    covered = np.zeros(n, dtype=int)
+    for a, b, Bp, C, comm in run_virtual(world, body):
+        assert np.array_equal(Bp.astype(np.float64), Bref[a:b])
+        assert np.array_equal(C.astype(np.float64), Cref)
+        assert comm == predicted_bytes_per_rank(n, r, layout, True, variant)
+        covered[a:b] += 1
+    assert np.all(covered == 1)

@@ -503,3 +503,75 @@ def test_three_pair_clusters_block_offsets(k0, capfd, monkeypatch):
     rows = np.concatenate([np.arange(0, 16), np.linspace(16, n1 - 1, 32).astype(int)])
     ref = oracle.sketch(SEED, "gaussian", A[rows], r, k0=k0)
     assert _relF(Bp.cpu().numpy()[rows], ref) <= TOL["bf16"]
+
+
+# ----------------------------------------------------------------------------- in-GEMM Omega, elementwise
+def _tf32_rna(x):
+    """fp32 -> tf32 round-to-nearest, ties away from zero (cvt.rna.tf32.f32; reading R7)."""
+    b = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((b + 0x1000) & 0xFFFFE000).astype(np.uint32).view(np.float32)
+
+
+def _bf16_rne(x):
+    """fp32 -> bf16 round-to-nearest-even (reading R8)."""
+    b = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000).astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "uniform"])
+@pytest.mark.parametrize("mode", ["tf32", "tf32x3", "bf16"])
+def test_identity_exposes_in_gemm_omega(dist, mode):
+    """A = I makes B the Omega tiles the GEMM generated and multiplied, element by element:
+    tf32: B == RNA_tf32(omega) exactly; bf16: B == RNE_bf16(omega) exactly; tf32x3 (Omega_hi + Omega_lo):
+    within 4 ulp of the fp32 omega -- with omega from the oracle, so the Philox counters, the Box-Muller /
+    uniform transform, the row/column mapping, the swizzled tile layout and the cluster sharing of the
+    slices are all checked (n = 2100 takes clusters of 4 CTA pairs in tf32 / bf16; r = 300 two passes)."""
+    sk = _sk()
+    n, r = 2100, 300
+    s = sk.Sketch(SEED, dist, n, r, mode=mode)
+    B = s.apply(_dev(np.eye(n, dtype=np.float32))).cpu().numpy()
+    om = oracle.omega(SEED, dist, 0, n, 0, r).astype(np.float32)
+    if mode == "tf32x3":
+        assert _ulp(B, om).max() <= 4
+    else:
+        rnd = _tf32_rna if mode == "tf32" else _bf16_rne
+        if dist == "uniform":
+            assert np.array_equal(B, rnd(om))  # uniforms are bit-exact, so their rounding is too
+        else:
+            # Gaussians: device value within 2 ulp, then rounded -> equal, or one rounding step apart
+            step = 2.0 ** (-10 if mode == "tf32" else -7)
+            err = np.abs(B.astype(np.float64) - rnd(om)) / np.maximum(np.abs(om), 2.0 ** -30)
+            assert np.mean(B == rnd(om)) > 0.999
+            assert err.max() <= step
+
+
+@pytest.mark.parametrize("mode", ["tf32", "tf32x3", "bf16"])
+def test_uniform_omega_sketch_and_core(mode):
+    """The paper's experimental Omega is uniform Philox: B and C through the GEMMs."""
+    sk = _sk()
+    n, r = 1500, 96
+    A = synth.symmetric_uniform(11, n)
+    s = sk.Sketch(SEED, "uniform", n, r, mode=mode)
+    B, C = s.nystrom_core(_dev(A))
+    Bref, Cref = oracle.nystrom_core(SEED, "uniform", A, r)
+    assert _relF(B.cpu().numpy(), Bref) <= TOL[mode]
+    assert _relF(C.cpu().numpy(), Cref) <= TOL[mode]
+    B2 = s.apply(_dev(synth.uniform(12, 700, n))).cpu().numpy()
+    assert _relF(B2, oracle.sketch(SEED, "uniform", synth.uniform(12, 700, n), r)) <= TOL[mode]
+
+
+@pytest.mark.parametrize("mode,omega", [("bf16", "fast"), ("tf32", "accurate")])
+def test_c4_shape_sampled_rows(mode, omega):
+    """c4's shape class: short-wide A 2048 x 2^19, r = 512 Gaussian (the full c4 has K = 4,000,000),
+    in the launch configuration the bench uses (clusters of CTA pairs over all 2048 rows); sampled
+    rows of B against the oracle."""
+    sk = _sk()
+    n1, n2, r = 2048, 1 << 19, 512
+    Ad = synth.uniform_device(4, n1, n2)
+    s = sk.Sketch(SEED, "gaussian", n2, r, mode=mode, omega=omega)
+    B = s.apply(Ad)
+    torch.cuda.synchronize()
+    rows = [0, 1, 127, 128, 511, 1024, 1500, 2047]
+    Bref = oracle.sketch(SEED, "gaussian", Ad[rows].cpu().numpy(), r)
+    assert _relF(B[rows].cpu().numpy(), Bref) <= TOL[mode]
+    del Ad
