@@ -231,9 +231,10 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int nsm = workers;  // independent workers (CTAs, CTA pairs or clusters of pairs)
     // The tensor core accumulates fp32 in TMEM with a bias toward zero of ~2^-24 per K=8 MMA step
     // (measured: relF = 7e-9 x K per accumulator, tools/acc_test.py).  tf32x3 promises fp32
-    // accuracy (1e-5), so it caps K per accumulator at 1024 (32 K-iterations) with split-K; the
-    // partials are summed in fp32 round-to-nearest.
-    const int min_split = x3 ? (P.kiters + 31) / 32 : 1;
+    // accuracy (1e-5), so it caps K per accumulator at 1024 (32 K-iterations) INSIDE the kernel: the
+    // epilogue drains TMEM every kchunk iterations and adds the chunk into the unit's output in fp32
+    // round-to-nearest (sketch_gemm.cu, `drain`), so any split / stream-K range keeps the cap.
+    const int min_split = 1;
     int best_s = 1;
     if (force_split > 0) {
         best_s = std::min(force_split, std::max(1, P.kiters));
@@ -258,9 +259,6 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     }
     if (best_s > 1 && force_split == 0 && ws_cap < static_cast<size_t>(best_s) * P.ws_per_split)
         best_s = std::max<int>(1, static_cast<int>(ws_cap / P.ws_per_split));
-    // tf32x3's accuracy cap holds whatever asked for the split (override, fused reduce-scatter, a
-    // short workspace: the caller's workspace_size covers min_split partials)
-    best_s = std::max(best_s, std::min(min_split, std::max(1, P.kiters)));
     // each split must own >= 1 K iteration
     const int kper = (P.kiters + best_s - 1) / best_s;
     P.split = (P.kiters + kper - 1) / kper;
@@ -270,9 +268,9 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     P.sk_len = 0;
     // Stream-K: every worker gets the same number of K iterations of the flattened (m-block, K)
     // space, cut at m-block boundaries, when wave quantisation of the split-K units would leave
-    // workers idle (e.g. 13 m-blocks on 15 clusters).  Not for tf32x3 (K per accumulator is capped)
-    // or an explicit split (fused reduce-scatter slots, tests).
-    if (!x3 && force_split == 0 && h->split_override == 0 && getenv("SK_NO_STREAMK") == nullptr && best < 1e299) {
+    // workers idle (e.g. 13 m-blocks on 15 clusters).  Not for an explicit split (fused
+    // reduce-scatter slots, tests).
+    if (force_split == 0 && h->split_override == 0 && getenv("SK_NO_STREAMK") == nullptr && best < 1e299) {
         const int64_t total = static_cast<int64_t>(P.num_mblk) * P.kiters;
         const int64_t L = (total + nsm - 1) / nsm;
         const int pieces = static_cast<int>((P.kiters + L - 1) / L) + 1;
@@ -318,21 +316,25 @@ CorePlan plan_core_simt(const sk_sketch_s* h, int64_t m) {
     return C;
 }
 
-// tcgen05 core for r <= 256 (one CTA per 128-aligned chunk of about m / #SMs rows); SIMT otherwise.
-CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0) {
-    // tf32x3 keeps C fp32-accurate with the fp32-FMA core (a 3xTF32 core is future work)
-    if (h->core_simt || h->mode == sk::kTF32x3) return plan_core_simt(h, m);
+// tcgen05 core: one CTA per (128-aligned chunk of B rows, block of C); SIMT only on request.
+// tf32 / bf16: blocks of up to 256 x 256, about one wave of CTAs.  tf32x3 (3xTF32): 128 x 128 blocks
+// (the hi + lo operands double the ring) and chunks of <= 1024 rows -- the TMEM accumulation
+// truncates (~7e-9 relative per accumulated K), so K per accumulator is capped as in
+// the sketch GEMM and the partials are summed in fp32 round-to-nearest by core_reduce.
+CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0, int64_t nb = -1) {
+    if (h->core_simt) return plan_core_simt(h, m);
+    if (nb < 0) nb = h->r;
+    const bool x3 = h->mode == sk::kTF32x3;
     CorePlan C{};
     C.tc = true;
-    // r or nb > 256: 256 x 256 blocks of C, one CTA per (row chunk, block); the chunk count shrinks
-    // so that the grid stays about one wave
-    C.npad = static_cast<int>(std::min<int64_t>(256, round_up(h->r, 16)));
-    C.nacc = h->r > 128 ? 2 : 1;
+    C.npad = static_cast<int>(std::min<int64_t>(x3 ? 128 : 256, round_up(nb, 16)));
+    C.nacc = (!x3 && h->r > 128) ? 2 : 1;
     C.base = i0 & ~static_cast<int64_t>(127);
     const int64_t span = std::max<int64_t>(1, i0 + m - C.base);
-    const int64_t blocks = ((h->r + 255) / 256) * ((h->r + 255) / 256);
+    const int64_t blocks = ((h->r + 128 * C.nacc - 1) / (128 * C.nacc)) * ((nb + C.npad - 1) / C.npad);
     const int64_t want = std::max<int64_t>(1, sk::num_sms() / blocks);
     C.step = round_up((span + want - 1) / want, 128);
+    if (x3) C.step = std::min<int64_t>(C.step, 1024);
     C.chunks = static_cast<int>((span + C.step - 1) / C.step);
     return C;
 }
@@ -340,6 +342,7 @@ CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0) {
 size_t core_ws_bytes(const sk_sketch_s* h, int64_t m) {
     // chunk count of either plan for any block offset (an unaligned i0 adds at most one chunk)
     const int64_t chunks = std::max<int64_t>(plan_core(h, m, 127).chunks + 1, plan_core_simt(h, m).chunks);
+    // (plan_core with nb = r: narrower column blocks -- core_apply_block_cols -- have as many chunks or fewer)
     return static_cast<size_t>(chunks) * h->r * h->r * sizeof(float);
 }
 
@@ -377,8 +380,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
     const int roff = static_cast<int>(k0 & 3);
     const SketchPlan P = plan_sketch(h, m, k, kshift, rs ? ~size_t(0) : ws_bytes, rs ? rs->split : 0);
     if (rs && (P.npass != 1 || P.split != rs->split))
-        return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256, split <= K iterations and, in "
-                                        "tf32x3, split >= sketch_rs_split (K per accumulator <= 1024)");
+        return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256 and split <= K iterations");
     CUtensorMap map;
     sk_status_t st = make_map_2d(&map, A, m, k, lda, 32, 128);
     if (st != SK_SUCCESS) return st;
@@ -400,6 +402,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         p.o_stages = P.o_stages;
         p.y_stages = P.y_stages;
         p.prefetch = 0;
+        p.kchunk = (h->mode == sk::kTF32x3) ? 1024 / 32 : 0;  // tf32x3: <= 1024 K per TMEM accumulation
         p.sk_len = P.sk_len;
         if (const char* e = getenv("SK_PREFETCH")) p.prefetch = std::max(0, std::min(16, atoi(e)));  // tuning
         p.key0 = static_cast<uint32_t>(h->seed);
@@ -451,7 +454,7 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
 sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, int64_t i0,
                       float* C, int64_t ldc, void* ws, cudaStream_t stream, int64_t nb = -1) {
     if (nb < 0) nb = h->r;
-    CorePlan CP = plan_core(h, m, i0);
+    CorePlan CP = plan_core(h, m, i0, nb);
     if (CP.tc && (!aligned16(B) || (ldb & 3))) CP = plan_core_simt(h, m);  // TMA needs 16-B rows
     if (CP.tc && m > 0) {
         CUtensorMap map;
@@ -465,7 +468,7 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         q.m = static_cast<int32_t>(m);
         q.r = static_cast<int32_t>(h->r);
         q.nb = static_cast<int32_t>(nb);
-        q.npad = static_cast<int32_t>(std::min<int64_t>(256, round_up(nb, 16)));
+        q.npad = CP.npad;
         q.nchunks = CP.chunks;
         q.key0 = static_cast<uint32_t>(h->seed);
         q.key1 = static_cast<uint32_t>(h->seed >> 32);
@@ -481,7 +484,8 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         cudaError_t e;
         {
             LaunchScope ls(h, SK_PHASE_CORE_GEMM, stream);
-            e = sk::launch_core_gemm_tc(map, omap, q, CP.nacc, h->dist, h->omega_transform == SK_OMEGA_FAST, stream);
+            e = sk::launch_core_gemm_tc(map, omap, q, CP.nacc, h->dist, h->omega_transform == SK_OMEGA_FAST,
+                                        h->mode == sk::kTF32x3, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "core_gemm_tc launch");
         {

@@ -2,9 +2,11 @@
 // "C-bar_j'k' = Omega^T_i'j' * B_i'k'"), with the Omega rows REGENERATED bit-identically to the
 // ones the sketch GEMM used (Alg. 2 regenerates rather than reuses; reading R16).
 //
-// v1: fp32 SIMT tiles (64 x 64 outputs per CTA, 32-row K steps through shared memory), K split
-// into `chunks` contiguous row ranges, one r x r partial per chunk, reduced in fixed order by
-// core_reduce_kernel.  fp32 FMA accumulation makes C at least as accurate as B in every mode.
+// Two implementations: core_gemm_tc_kernel (tcgen05, below: kind::tf32 in the tf32 / bf16 modes,
+// 3xTF32 in tf32x3) is the product path; core_gemm_simt_kernel (fp32 FMA tiles, 64 x 64 outputs per
+// CTA, 32-row K steps through shared memory) is kept for B blocks TMA cannot address (unaligned
+// base or row stride) and as sketch_set_core_impl(h, 1).  Both split K into contiguous row chunks,
+// one r x r partial per chunk, reduced in fixed order by core_reduce_kernel.
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -114,6 +116,10 @@ cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaS
 // partial of its K-chunk of B rows (one block when r, nb <= 256).
 //   D[a, b] += OmegaT[a, i] * B[i, b]:  M = Omega columns a (NACC blocks of 128), N = npad (b),
 //   K = rows i in 32-row steps, kind::tf32, fp32 accumulators in TMEM.
+//   * tf32x3 (MODE == kTF32x3): Omega^T = hi + lo and B = hi + lo (hi = tf32 RN, lo = x - hi exact),
+//     three MMAs per K step (lo*hi, hi*lo, hi*hi; Rademacher Omega is exact: two); one 128 x 128
+//     block per CTA (the doubled operands fill the ring) and <= 1024 rows of K per chunk, because the
+//     TMEM accumulation truncates: C stays fp32-accurate.
 //   * Omega^T tile (A operand, K-major SW128) is regenerated by 16 producer warps with the sketch
 //     GEMM's tile writer (bit-identical Omega).
 //   * B tile: TMA loads row-major B (boxes of 32 rows x 32 columns, no swizzle) into a raw ring;
@@ -138,11 +144,12 @@ constexpr int kCoreRawStages = 2;  // raw B ring (TMA)
 struct CoreSmem {
     uint32_t raw_stage, o_stage, bt_stage, raw_off, o_off, bt_off, epi_off, bar_off, total;
 };
-__host__ __device__ inline CoreSmem core_smem(int nacc, int npad) {
+// x3: Omega^T and B^T tiles each followed by their lo tile (olo: Omega_lo present)
+__host__ __device__ inline CoreSmem core_smem(int nacc, int npad, bool x3 = false, bool olo = false) {
     CoreSmem L;
     L.raw_stage = static_cast<uint32_t>((npad + 31) / 32) * 4096u;
-    L.o_stage = static_cast<uint32_t>(nacc) * 16384u;
-    L.bt_stage = static_cast<uint32_t>(npad) * 128u;
+    L.o_stage = static_cast<uint32_t>(nacc) * 16384u * (olo ? 2u : 1u);
+    L.bt_stage = static_cast<uint32_t>(npad) * 128u * (x3 ? 2u : 1u);
     L.raw_off = 0;
     L.o_off = L.raw_off + kCoreRawStages * L.raw_stage;
     L.bt_off = L.o_off + kCoreStages * L.o_stage;
@@ -159,7 +166,11 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    const CoreSmem L = core_smem(NACC, p.npad);
+    constexpr bool X3 = (MODE == kTF32x3);
+    constexpr bool OLO = X3 && (DIST != kRademacher);  // +-1 is exact in tf32: no Omega_lo
+    const CoreSmem L = core_smem(NACC, p.npad, X3, OLO);
+    const uint32_t o_lo = NACC * 16384u;                               // Omega_lo tile offset
+    const uint32_t b_lo = static_cast<uint32_t>(p.npad) * 128u;        // B_lo tile offset
     uint8_t* sRaw = smem + L.raw_off;
     uint8_t* sO = smem + L.o_off;
     uint8_t* sBt = smem + L.bt_off;
@@ -173,8 +184,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
 
     const uint32_t warp = warp_id(), lane = lane_id();
     const int chunk = blockIdx.x;
-    const int a_off = static_cast<int>(blockIdx.y) * 256;  // first Omega column (row of C) of this block
-    const int b_off = static_cast<int>(blockIdx.z) * 256;  // first column of B / C of this block
+    const int a_off = static_cast<int>(blockIdx.y) * 128 * NACC;  // first Omega column (row of C) of this block
+    const int b_off = static_cast<int>(blockIdx.z) * p.npad;      // first column of B / C of this block
     const int64_t g0 = p.base + static_cast<int64_t>(chunk) * p.step;  // aligned global row
     const int64_t gend = min(p.i0 + static_cast<int64_t>(p.m), g0 + p.step);
     const int ksteps = static_cast<int>((gend - g0 + 31) / 32);
@@ -223,7 +234,18 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
 #pragma unroll
                     for (int a = 0; a < NACC; ++a) {
                         const uint64_t adesc = sw128_desc(o_base + a * 16384 + k8 * 32, 16, 1024);
-                        mma_tf32(tmem_base + a * p.npad, adesc, bdesc, idesc, (t > 0 || k8 > 0) ? 1u : 0u);
+                        const uint32_t d = tmem_base + a * p.npad;
+                        uint32_t acc = (t > 0 || k8 > 0) ? 1u : 0u;
+                        if constexpr (X3) {
+                            // small terms first: Omega_lo * B_hi, Omega_hi * B_lo, then hi * hi
+                            if constexpr (OLO) {
+                                mma_tf32(d, sw128_desc(o_base + o_lo + a * 16384 + k8 * 32, 16, 1024), bdesc, idesc, acc);
+                                acc = 1u;
+                            }
+                            mma_tf32(d, adesc, sw128_desc(bt_base + b_lo + k8 * 32, 16, 1024), idesc, acc);
+                            acc = 1u;
+                        }
+                        mma_tf32(d, adesc, bdesc, idesc, acc);
                     }
                 }
                 mma_commit(&empty_op[so]);
@@ -241,10 +263,10 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             mbar_wait(&empty_op[so], po ^ 1);
             uint8_t* o_tile = sO + so * L.o_stage;
             if constexpr (DIST == kRademacher)
-                produce_omega_tile_r<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, a_off, p.key0, p.key1, tt);
+                produce_omega_tile_r<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, a_off, p.key0, p.key1, tt, o_lo);
             else
                 produce_omega_tile_g<DIST, MODE, FAST>(o_tile, g0 + 32 * t, 0, nrows, a_off, p.key0, p.key1,
-                                                       n_start, j_start, tq, tr);
+                                                       n_start, j_start, tq, tr, o_lo);
             // transpose the raw B tile (32 rows i x npad cols b, 128-B rows per 32-col group) into
             // the K-major SW128 tile: row b, chunk j4 = rows 4 j4 .. 4 j4 + 3
             mbar_wait(&full_raw[sr], pr);
@@ -253,14 +275,14 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             for (int c = tt; c < p.npad * 8; c += kCoreRng * 32) {
                 const int b = c % p.npad, j4 = c / p.npad;
                 const float* col = reinterpret_cast<const float*>(raw + (b >> 5) * 4096) + (b & 31);
-                float4 v = make_float4(col[(4 * j4 + 0) * 32], col[(4 * j4 + 1) * 32], col[(4 * j4 + 2) * 32],
-                                       col[(4 * j4 + 3) * 32]);
-                v.x = to_tf32(v.x); v.y = to_tf32(v.y); v.z = to_tf32(v.z); v.w = to_tf32(v.w);
+                const float4 v = make_float4(col[(4 * j4 + 0) * 32], col[(4 * j4 + 1) * 32],
+                                             col[(4 * j4 + 2) * 32], col[(4 * j4 + 3) * 32]);
+                const float4 h = make_float4(to_tf32(v.x), to_tf32(v.y), to_tf32(v.z), to_tf32(v.w));
                 const uint32_t addr = bt + static_cast<uint32_t>(b) * 128u +
                                       ((static_cast<uint32_t>(j4) ^ static_cast<uint32_t>(b & 7)) << 4);
-                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y),
-                             "f"(v.z), "f"(v.w)
-                             : "memory");
+                st_shared_v4(addr, h);
+                if constexpr (X3)  // B_lo = B - B_hi (exact in fp32)
+                    st_shared_v4(addr + b_lo, make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w));
             }
             fence_proxy_async_smem();
             __syncwarp();
@@ -317,22 +339,32 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
     }
 }
 
-size_t core_gemm_tc_smem_bytes(int nacc, int npad) { return core_smem(nacc, npad).total + 1024; }
+size_t core_gemm_tc_smem_bytes(int nacc, int npad, bool x3, bool olo) {
+    return core_smem(nacc, npad, x3, olo).total + 1024;
+}
 
 template <int NACC, int DIST, int MODE, bool FAST>
 static cudaError_t launch_core_tc_one(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
                                       cudaStream_t s) {
     auto kern = core_gemm_tc_kernel<NACC, DIST, MODE, FAST>;
-    const size_t smem = core_gemm_tc_smem_bytes(NACC, p.npad);
+    const size_t smem = core_gemm_tc_smem_bytes(NACC, p.npad, MODE == kTF32x3, MODE == kTF32x3 && DIST != kRademacher);
     if (cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(kern), smem)) return e;
-    const dim3 grid(p.nchunks, (p.r + 255) / 256, (p.nb + 255) / 256);
+    const dim3 grid(p.nchunks, (p.r + 128 * NACC - 1) / (128 * NACC), (p.nb + p.npad - 1) / p.npad);
     kern<<<grid, kCoreThreads, smem, s>>>(tmB, tmOut, p);
     return cudaGetLastError();
 }
 
 template <int NACC>
 static cudaError_t core_tc_dist(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
-                                int dist, bool fast, cudaStream_t s) {
+                                int dist, bool fast, bool x3, cudaStream_t s) {
+    if (x3) {  // 3xTF32, accurate Omega only (the fast transform is refused in tf32x3)
+        if constexpr (NACC == 1) {
+            if (dist == kRademacher) return launch_core_tc_one<1, kRademacher, kTF32x3, false>(tmB, tmOut, p, s);
+            if (dist == kUniform) return launch_core_tc_one<1, kUniform, kTF32x3, false>(tmB, tmOut, p, s);
+            return launch_core_tc_one<1, kGaussian, kTF32x3, false>(tmB, tmOut, p, s);
+        }
+        return cudaErrorNotSupported;
+    }
     if (dist == kRademacher) return launch_core_tc_one<NACC, kRademacher, kTF32, false>(tmB, tmOut, p, s);
     if (dist == kUniform) return launch_core_tc_one<NACC, kUniform, kTF32, false>(tmB, tmOut, p, s);
     if (fast) return launch_core_tc_one<NACC, kGaussian, kTF32, true>(tmB, tmOut, p, s);
@@ -340,9 +372,9 @@ static cudaError_t core_tc_dist(const CUtensorMap& tmB, const CUtensorMap& tmOut
 }
 
 cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
-                                int nacc, int dist, bool fast, cudaStream_t s) {
-    if (nacc == 1) return core_tc_dist<1>(tmB, tmOut, p, dist, fast, s);
-    if (nacc == 2) return core_tc_dist<2>(tmB, tmOut, p, dist, fast, s);
+                                int nacc, int dist, bool fast, bool x3, cudaStream_t s) {
+    if (nacc == 1) return core_tc_dist<1>(tmB, tmOut, p, dist, fast, x3, s);
+    if (nacc == 2) return core_tc_dist<2>(tmB, tmOut, p, dist, fast, x3, s);
     return cudaErrorNotSupported;
 }
 

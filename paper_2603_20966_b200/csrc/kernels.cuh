@@ -31,6 +31,8 @@ struct SketchGemmParams {
     int32_t o_stages;     // Omega smem pipeline depth
     int32_t y_stages;     // bf16: depth of the ring holding K 32..63 of each fp32 A stage
     int32_t prefetch;     // K steps of A prefetched into L2 ahead of the TMA loads (0 = off)
+    int32_t kchunk;       // > 0 (tf32x3): K iterations per TMEM accumulation; each chunk is drained
+                          // and added (fp32 RN) into the unit's output, which accumulates in place
     int64_t sk_len;       // > 0: stream-K -- worker w runs flattened (m-block, K-iteration) indices
                           // [w sk_len, (w+1) sk_len), cut at m-block boundaries; partial `piece` =
                           // w - first worker touching the m-block (split / kper unused)
@@ -73,7 +75,7 @@ struct CoreTcParams {
     int32_t m;            // rows of B
     int32_t r;            // Omega columns = rows of C
     int32_t nb;           // columns of B = columns of C
-    int32_t npad;         // MMA N = nb padded (multiple of 16, <= 256)
+    int32_t npad;         // MMA N = columns per block (multiple of 16, <= 256; <= 128 in tf32x3)
     int32_t nchunks;
     int32_t tma_store;    // 1: epilogue stores 32x32 tiles with TMA through tmOut (r % 32 == 0)
     uint32_t key0, key1;
@@ -110,8 +112,8 @@ cudaError_t launch_splitk_reduce(const float* part, int64_t part_stride, int32_t
 
 cudaError_t launch_core_gemm(const CoreGemmParams& p, int dist, bool fast, cudaStream_t s);
 cudaError_t launch_core_gemm_tc(const CUtensorMap& tmB, const CUtensorMap& tmOut, const CoreTcParams& p,
-                                int nacc, int dist, bool fast, cudaStream_t s);
-size_t core_gemm_tc_smem_bytes(int nacc, int npad);
+                                int nacc, int dist, bool fast, bool x3, cudaStream_t s);
+size_t core_gemm_tc_smem_bytes(int nacc, int npad, bool x3, bool olo);
 cudaError_t launch_accumulate(float* acc, const float* part, int64_t n, bool first, cudaStream_t s);
 cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, int32_t nb, float* C,
                                int64_t ldc, cudaStream_t s);

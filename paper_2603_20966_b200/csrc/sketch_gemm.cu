@@ -232,6 +232,71 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         return static_cast<int>((static_cast<uint32_t>(rows) * q) / static_cast<uint32_t>(CL));
     };
     const int pair_row0 = static_cast<int>(pairq) * 128 * CG * NACC;  // this pair's rows inside a unit
+    const int kchunk = p.kchunk > 0 ? p.kchunk : 0x7fffffff;          // K iterations per accumulation
+
+    // Epilogue of one accumulation chunk, by the warp reading TMEM lane quadrant q (lanes 32q..32q+31 =
+    // rows of this CTA's 128-row tiles): tcgen05.ld -> the unit's output row (B, the split / stream-K
+    // partial `s`, or a peer's receive slot) -- stored for the first chunk of the unit, added (fp32 RN,
+    // same thread every time: a fixed order) for later ones -- then TMEM is handed back to the MMA.
+    auto drain = [&](uint32_t q, int mb, int s, bool first, uint32_t nd) {
+        mbar_wait(tmem_full, nd & 1);
+        tc_fence_after();
+        float* out = p.out + ((p.split > 1 || p.sk_len > 0) ? static_cast<int64_t>(s) * p.part_stride : 0);
+        const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+#pragma unroll 1
+        for (int a = 0; a < NACC; ++a) {
+            const int row = mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128 +
+                            static_cast<int>(q) * 32 + static_cast<int>(lane);
+            float* orow = out + static_cast<int64_t>(row) * p.ldo;
+            if (p.rs_ndst > 0 && row < p.n1) {
+                // fused reduce-scatter: the row's partial goes straight to its owner's slot
+                // (NVLink store into the peer's receive buffer), no local B / split partial
+                const int64_t piece = row / p.rs_piece;
+                orow = p.rs_dst[piece] + (static_cast<int64_t>(p.rs_slot) * p.split + s) * p.rs_slot_elems +
+                       (row - piece * p.rs_piece) * p.ldo;
+            }
+#pragma unroll 1
+            for (int cc = 0; cc < p.npad; cc += 32) {
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(a * p.npad + cc);
+                uint32_t v[32];
+                if (cc + 32 <= p.npad) {
+                    tmem_ld_32x32b_x32(taddr, v);
+                } else {
+                    uint32_t h[16];
+                    tmem_ld_32x32b_x16(taddr, h);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) { v[i] = h[i]; v[16 + i] = 0u; }
+                }
+                tmem_ld_wait();
+                if (row < p.n1) {
+                    if (vec_ok && cc + 32 <= p.r_valid) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                   __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+                            float4* dst = reinterpret_cast<float4*>(orow + cc + i);
+                            if (!first) {
+                                const float4 b = *dst;
+                                o.x = b.x + o.x; o.y = b.y + o.y; o.z = b.z + o.z; o.w = b.w + o.w;
+                            }
+                            *dst = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (cc + i < p.r_valid)
+                                orow[cc + i] = first ? __uint_as_float(v[i]) : orow[cc + i] + __uint_as_float(v[i]);
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(tmem_empty), lead_rank));
+            else mbar_arrive(tmem_empty);
+        }
+    };
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer
@@ -307,13 +372,16 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // ------------------------------------------------------------------ MMA issuer (leader)
         if (elect_one()) {
             const uint32_t idesc = make_idesc(BF ? kFmtBF16 : kFmtTF32, 128 * CG, static_cast<uint32_t>(p.npad), 0, 0);
-            uint32_t sa = 0, pa = 0, so = 0, po = 0, local = 0, ntr = 0;
+            uint32_t sa = 0, pa = 0, so = 0, po = 0, nd = 0, ntr = 0;
             WorkIter wi(p, group);
             int mb, kb, ke, s;
-            for (; wi.next(p, ngroups, mb, kb, ke, s); ++local) {
-                mbar_wait(tmem_empty, (local & 1) ^ 1);
-                tc_fence_after();
+            while (wi.next(p, ngroups, mb, kb, ke, s)) {
                 for (int kit = kb; kit < ke; ++kit, ++ntr) {
+                    const int ci = (kit - kb) % kchunk;  // K iteration inside the accumulation chunk
+                    if (ci == 0) {  // the epilogue has drained the previous chunk
+                        mbar_wait(tmem_empty, (nd & 1) ^ 1);
+                        tc_fence_after();
+                    }
                     if constexpr (XA) mbar_wait(&conv[sa], pa);  // both CTAs' A stage converted
                     else mbar_wait(&full_a[sa], pa);
                     trace_stamp(p, 1, ntr);
@@ -329,7 +397,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
 #pragma unroll
                         for (int a = 0; a < NACC; ++a) {
                             const uint64_t adesc = sw128_desc(a_base + (a * NBOX + sub) * kATileBytes + kk * 32, 16, 1024);
-                            uint32_t acc = (kit > kb || k8 > 0) ? 1u : 0u;
+                            uint32_t acc = (ci > 0 || k8 > 0) ? 1u : 0u;
                             const uint32_t d = tmem_base + a * p.npad;
                             if constexpr (X3) {
                                 // small terms first: A_lo * Omega_hi, A_hi * Omega_lo, then A_hi * Omega_hi
@@ -364,9 +432,12 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     }
                     if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                     if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
+                    if (ci == kchunk - 1 || kit + 1 == ke) {  // chunk complete: hand TMEM to the epilogue
+                        if constexpr (CG == 2) mma_commit_pair(tmem_full, pair_mask);
+                        else mma_commit(tmem_full);
+                        ++nd;
+                    }
                 }
-                if constexpr (CG == 2) mma_commit_pair(tmem_full, pair_mask);
-                else mma_commit(tmem_full);
             }
         }
     } else if (warp == 2 || warp == 3 || (warp == 1 && !leader)) {
@@ -437,11 +508,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         const int n_start = tt % gen_rows, j_start = tt / gen_rows;
         const int tq = nthr / gen_rows, tr = nthr % gen_rows;
         const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
-        uint32_t so = 0, po = 0, sa = 0, pa = 0, local = 0, ntr = 0;
+        uint32_t so = 0, po = 0, nd = 0, ntr = 0;
         const uint32_t lo_off = L.olo_off - L.ohi_off;
         WorkIter wi(p, group);
         int mb, kb, ke, s;
-        for (; wi.next(p, ngroups, mb, kb, ke, s); ++local) {
+        while (wi.next(p, ngroups, mb, kb, ke, s)) {
             for (int kit = kb; kit < ke; ++kit, ++ntr) {
                 if (p.ablate & 32u) mbar_wait(&empty_o[so], po ^ 1);
                 else mbar_wait_sleep(&empty_o[so], po ^ 1);
@@ -489,60 +560,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 }
                 if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
             }
-            if (t < 128) {
+            if (!X3 && t < 128) {
                 // epilogue: warp (4+q) reads TMEM lanes 32q..32q+31 = rows of this CTA's half
-                const int q = t >> 5;
-                mbar_wait(tmem_full, local & 1);
-                tc_fence_after();
-                float* out = p.out + ((p.split > 1 || p.sk_len > 0) ? static_cast<int64_t>(s) * p.part_stride : 0);
-                const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-#pragma unroll 1
-                for (int a = 0; a < NACC; ++a) {
-                    const int row = mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128 +
-                                    q * 32 + static_cast<int>(lane);
-                    float* orow = out + static_cast<int64_t>(row) * p.ldo;
-                    if (p.rs_ndst > 0 && row < p.n1) {
-                        // fused reduce-scatter: the row's partial goes straight to its owner's slot
-                        // (NVLink store into the peer's receive buffer), no local B / split partial
-                        const int64_t piece = row / p.rs_piece;
-                        orow = p.rs_dst[piece] + (static_cast<int64_t>(p.rs_slot) * p.split + s) * p.rs_slot_elems +
-                               (row - piece * p.rs_piece) * p.ldo;
-                    }
-#pragma unroll 1
-                    for (int cc = 0; cc < p.npad; cc += 32) {
-                        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                               static_cast<uint32_t>(a * p.npad + cc);
-                        uint32_t v[32];
-                        if (cc + 32 <= p.npad) {
-                            tmem_ld_32x32b_x32(taddr, v);
-                        } else {
-                            uint32_t h[16];
-                            tmem_ld_32x32b_x16(taddr, h);
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) { v[i] = h[i]; v[16 + i] = 0u; }
-                        }
-                        tmem_ld_wait();
-                        if (row < p.n1) {
-                            if (vec_ok && cc + 32 <= p.r_valid) {
-#pragma unroll
-                                for (int i = 0; i < 32; i += 4)
-                                    *reinterpret_cast<float4*>(orow + cc + i) =
-                                        make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                    __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-                            } else {
-#pragma unroll
-                                for (int i = 0; i < 32; ++i)
-                                    if (cc + i < p.r_valid) orow[cc + i] = __uint_as_float(v[i]);
-                            }
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(tmem_empty), lead_rank));
-                    else mbar_arrive(tmem_empty);
-                }
+                drain(static_cast<uint32_t>(t >> 5), mb, s, true, nd);
+                ++nd;
             }
         }
     } else if constexpr (X3) {
@@ -550,9 +571,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         // A_lo = A - trunc_tf32(A) (exact in fp32), elementwise next to the TMA'd A tiles of the same
         // stage (same SW128 layout, so the copy is layout-agnostic); the MMA reads A (as tf32, i.e.
         // truncated) and A_lo.  In their own warps this overlaps the Omega generation.
+        // They also run the epilogue: after converting the last stage of each accumulation chunk
+        // (kchunk K iterations) they drain TMEM into the unit's output (first chunk: store; later
+        // chunks: add in fp32 round-to-nearest -- the promotion that keeps the truncating TMEM
+        // accumulation to <= 1024 K), while the producers run ahead.
         const int cw = static_cast<int>(warp) - (kCtlWarps + kRngW);
         const int ct = cw * 32 + static_cast<int>(lane);
-        uint32_t sa = 0, pa = 0;
+        uint32_t sa = 0, pa = 0, nd = 0;
         WorkIter wi(p, group);
         int mb, kb, ke, s;
         while (wi.next(p, ngroups, mb, kb, ke, s)) {
@@ -579,6 +604,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     else mbar_arrive(&conv[sa]);
                 }
                 if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
+                const int ci = (kit - kb) % kchunk;
+                if (ci == kchunk - 1 || kit + 1 == ke) {
+                    drain(static_cast<uint32_t>(cw), mb, s, kit - kb < kchunk, nd);
+                    ++nd;
+                }
             }
         }
     } else if constexpr (BF) {

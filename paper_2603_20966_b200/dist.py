@@ -433,11 +433,9 @@ class DistSketch:
         if self._rs is None or self._rs["key"] != (rows, per, k):
             # split-K partials would each cross NVLink (S x the reduce-scatter bytes): default to no
             # split; SK_RS_SPLIT=auto takes the local plan's choice (max over the row group)
-            # tf32x3 caps K per TMEM accumulator: at least the local plan's split there
-            x3 = getattr(self.local, "mode", None) == "tf32x3"
             env = os.environ.get("SK_RS_SPLIT", "1")
             split = 1 if env == "auto" else max(1, int(env))
-            if env == "auto" or x3:
+            if env == "auto":
                 t = torch.tensor([max(split, self.local.rs_split(rows, k))], dtype=torch.int32, device=A_blk.device)
                 self.row_comm.all_reduce(t, op="max")  # same slot layout everywhere
                 split = int(t.item())

@@ -547,10 +547,11 @@ def test_identity_exposes_in_gemm_omega(dist, mode):
 
 @pytest.mark.parametrize("mode", ["tf32", "tf32x3", "bf16"])
 def test_uniform_omega_sketch_and_core(mode):
-    """The paper's experimental Omega is uniform Philox: B and C through the GEMMs."""
+    """The paper's experimental Omega is uniform Philox: B and C through the GEMMs, on
+    an RBF kernel matrix as in the paper's experiments."""
     sk = _sk()
     n, r = 1500, 96
-    A = synth.symmetric_uniform(11, n)
+    A = synth.rbf_kernel(11, n, 64)
     s = sk.Sketch(SEED, "uniform", n, r, mode=mode)
     B, C = s.nystrom_core(_dev(A))
     Bref, Cref = oracle.nystrom_core(SEED, "uniform", A, r)

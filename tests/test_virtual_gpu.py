@@ -78,7 +78,7 @@ def test_virtual_layouts_nystrom_exact(world, spec, rs):
     from paper_2603_20966_b200.dist import Layout, predicted_bytes_per_rank
     if rs != "nccl" and Layout.parse(spec, world).p2 == 1:
         pytest.skip("no reduce-scatter in the row-block layout")
-    n, r = 1100, 48
+    n, r = 1120, 48  # n / p1 divisible by p2 on every grid: no padded rows in the exchanged pieces
     A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
     Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
     res = _run(world, spec, n, n, r, "rademacher", "tf32", A, rs=rs, fused_ar=True)
