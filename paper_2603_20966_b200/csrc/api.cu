@@ -133,8 +133,9 @@ int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // ---------------------------------------------------------------------------- launch planning
 struct SketchPlan {
-    int npass;         // column passes of <= 256 columns
-    int npad[32];      // MMA N per pass
+    int npass;         // column passes of <= 256 columns (<= 512 with ncol = 2)
+    int npad[32];      // MMA N per pass (per column block with ncol = 2)
+    int ncol;          // 2: one A tile against two N = 256 Omega column blocks per pass
     int cg;            // 1: one CTA per tile; 2: CTA pair (tcgen05 cta_group::2, M = 256)
     int cl;            // 2: clusters of two CTA pairs sharing every generated Omega slice
     int nacc;
@@ -150,18 +151,39 @@ struct SketchPlan {
 };
 
 SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, size_t ws_cap,
-                       int force_split = 0) {
+                       int force_split = 0, bool allow_ncol = true);
+SketchPlan plan_sketch_ncol1(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, size_t ws_cap, int force_split) {
+    return plan_sketch(h, n1, k, kshift, ws_cap, force_split, false);
+}
+
+SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, size_t ws_cap,
+                       int force_split, bool allow_ncol) {
     SketchPlan P{};
     const int64_t rpad = round_up(h->r, 16);
-    P.npass = static_cast<int>((rpad + 255) / 256);
-    int npad_max = 0;
-    for (int i = 0; i < P.npass; ++i) {
-        P.npad[i] = static_cast<int>(std::min<int64_t>(256, rpad - 256 * i));
-        npad_max = std::max(npad_max, P.npad[i]);
-    }
+    const bool x3 = h->mode == sk::kTF32x3;
     P.cg = (n1 > 256 && h->cg_override != 1) ? 2 : 1;
     P.nacc = (n1 > 128 * P.cg) ? 2 : 1;
-    const bool x3 = h->mode == sk::kTF32x3;
+    // Wide r (256 < r <= 512, or r a multiple of 512): one pass over A per 512 columns -- each CTA
+    // holds ONE 128-row A tile against two N = 256 Omega column blocks (TMEM: 2 x 256 columns), in
+    // clusters of 8 CTA pairs (2048 rows share every generated Omega element) or 4; reading A once
+    // instead of twice per 512 columns.  Gaussian / uniform Omega, tf32 / bf16.
+    P.ncol = 1;
+    {
+        const char* e = getenv("SK_NCOL");  // tuning: SK_NCOL=1 forces 256-column passes
+        const bool want = allow_ncol && !(e && atoi(e) == 1) && h->cl_override == 0;
+        if (want && !x3 && h->dist != sk::kRademacher && P.cg == 2 && n1 > 512 && rpad > 256 &&
+            (rpad <= 512 || rpad % 512 == 0)) {
+            P.ncol = 2;
+            P.nacc = 1;
+        }
+    }
+    const int cols_per_pass = 256 * P.ncol;
+    P.npass = static_cast<int>((rpad + cols_per_pass - 1) / cols_per_pass);
+    int npad_max = 0;
+    for (int i = 0; i < P.npass; ++i) {
+        P.npad[i] = P.ncol == 2 ? 256 : static_cast<int>(std::min<int64_t>(256, rpad - 256 * i));
+        npad_max = std::max(npad_max, P.npad[i]);
+    }
     const bool bf = h->mode == sk::kBF16;
     const bool xa = x3 || bf;
     const bool t64 = (h->mode == sk::kTF32) && P.cg == 2;  // tf32 pairs run 64-wide K steps
@@ -173,7 +195,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     const int budget = sk::sketch_gemm_max_smem() - 2048;
     // operand stage: Omega (+ Omega_lo); tf32x3 keeps A_lo in the A stage, bf16 converts A in place
     auto ostage_bytes = [&](int) {
-        const int otile = (npad_max / P.cg) * 128 * nsubo;
+        const int otile = (P.ncol * npad_max / P.cg) * 128 * nsubo;
         return otile * (olo ? 2 : 1);
     };
     int a_cap = 6;
@@ -189,11 +211,11 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
         const int y_bytes = P.y_stages * P.nacc * 128 * 32 * 4;
         P.a_stages = std::min(a_cap, (budget - y_bytes - 2 * ostage_bytes(P.nacc)) / a_slot);
         P.o_stages = std::max(2, std::min(P.o_stages, (budget - y_bytes - P.a_stages * a_slot) / ostage_bytes(P.nacc)));
-        if (P.a_stages >= 2 || P.nacc == 1) break;
+        if (P.a_stages >= 2 || P.nacc == 1 || P.ncol == 2) break;
         P.nacc = 1;  // make room for >= 2 A stages
     }
     const int a_stage = P.nacc * 128 * ks * 4;  // A bytes per K step
-    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo,
+    P.smem = sk::sketch_gemm_smem_bytes(P.cg, P.nacc, P.ncol * npad_max, P.a_stages, P.o_stages, x3, olo, ks, nsubo,
                                         P.y_stages);
     P.kiters = static_cast<int>((k + kshift + ks - 1) / ks);
     // Clusters of CTA pairs share each generated Gaussian Omega slice: every element then feeds
@@ -208,6 +230,12 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
         return P.cg == 2 && P.nacc == 2 && n1 >= 512 * cl && split_ok && h->dist == sk::kGaussian;
     };
     P.cl = 1;
+    const bool fast_t = h->omega_transform == SK_OMEGA_FAST;
+    if (P.ncol == 2) {
+        // 16-CTA clusters when the rows fill them (and the GPU packs them), else 8 CTAs
+        P.cl = (n1 > 1024 && sk::sketch_gemm_max_clusters(2, 1, h->dist, h->mode, fast_t, 8, P.smem, 2) > 0) ? 8 : 4;
+        if (const char* e = getenv("SK_NCOL_CL")) P.cl = atoi(e) == 8 ? 8 : 4;  // tuning
+    }
     // bf16 with the fast (MUFU) transform generates Omega cheaply enough that 3 pairs per cluster
     // win: clusters of 6 CTAs pack 22 per B200 (132 SMs) against 15 of 8 CTAs (120 SMs), at 4/3
     // the generated elements per A byte (c2: 2.05 -> 1.98 ms, 25000^2: 0.571 -> 0.538 ms, 12500 x
@@ -215,19 +243,30 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // 2.22 ms, 12500 x 50000 0.600 -> 0.631).  Only for n1 >= 4 units of 1536 rows, so the ragged
     // last unit stays a small share (c4, n1 = 2048, keeps one 2048-row unit).
     const bool fast = h->omega_transform == SK_OMEGA_FAST;
-    if (h->cl_override == 0 && !x3)
+    if (P.ncol == 2) {
+        // (chosen above)
+    } else if (h->cl_override == 0 && !x3) {
         P.cl = (bf && fast && n1 >= 4 * 1536 && cl_ok(3)) ? 3 : cl_ok(4) ? 4 : cl_ok(2) ? 2 : 1;
-    else if (h->cl_override >= 2) P.cl = cl_ok(h->cl_override) ? h->cl_override : 1;
+    } else if (h->cl_override >= 2) {
+        P.cl = cl_ok(h->cl_override) ? h->cl_override : 1;
+    }
     int workers = sk::num_sms() / P.cg;
     if (P.cl > 1) {
-        const int mc = sk::sketch_gemm_max_clusters(P.cg, P.nacc, h->dist, h->mode,
-                                                    h->omega_transform == SK_OMEGA_FAST, P.cl, P.smem);
-        if (mc <= 0) P.cl = 1;
-        else workers = std::min(mc, sk::num_sms() / (2 * P.cl));
+        int mc = sk::sketch_gemm_max_clusters(P.cg, P.nacc, h->dist, h->mode, fast_t, P.cl, P.smem, P.ncol);
+        if (mc <= 0 && P.ncol == 2 && P.cl == 8) {  // 16-CTA clusters do not fit: 8 CTAs
+            P.cl = 4;
+            mc = sk::sketch_gemm_max_clusters(P.cg, P.nacc, h->dist, h->mode, fast_t, P.cl, P.smem, P.ncol);
+        }
+        if (mc <= 0) {
+            if (P.ncol == 2) return plan_sketch_ncol1(h, n1, k, kshift, ws_cap, force_split);
+            P.cl = 1;
+        } else {
+            workers = std::min(mc, sk::num_sms() / (2 * P.cl));
+        }
     }
     const int rows_per_unit = 128 * P.cg * P.nacc * P.cl;
     P.num_mblk = static_cast<int>((n1 + rows_per_unit - 1) / rows_per_unit);
-    P.ws_per_split = static_cast<size_t>(n1) * npad_max * sizeof(float);
+    P.ws_per_split = static_cast<size_t>(n1) * npad_max * P.ncol * sizeof(float);
     const int nsm = workers;  // independent workers (CTAs, CTA pairs or clusters of pairs)
     // The tensor core accumulates fp32 in TMEM with a bias toward zero of ~2^-24 per K=8 MMA step
     // (measured: relF = 7e-9 x K per accumulator, tools/acc_test.py).  tf32x3 promises fp32
@@ -252,7 +291,7 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
             const int kper = (P.kiters + s - 1) / s;
             double t = static_cast<double>(waves) * (kper + unit_ovh);
             if (s > 1)
-                t += static_cast<double>(s + 1) * n1 * npad_max * 4.0 /
+                t += static_cast<double>(s + 1) * n1 * npad_max * P.ncol * 4.0 /
                      (static_cast<double>(nsm) * a_stage * P.cg);
             if (t < best * 0.995) { best = t; best_s = s; }
         }
@@ -270,12 +309,13 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // space, cut at m-block boundaries, when wave quantisation of the split-K units would leave
     // workers idle (e.g. 13 m-blocks on 15 clusters).  Not for an explicit split (fused
     // reduce-scatter slots, tests).
-    if (force_split == 0 && h->split_override == 0 && getenv("SK_NO_STREAMK") == nullptr && best < 1e299) {
+    if (force_split == 0 && h->split_override == 0 && getenv("SK_NO_STREAMK") == nullptr && best < 1e299 &&
+        P.num_mblk > 0 && P.kiters > 0) {
         const int64_t total = static_cast<int64_t>(P.num_mblk) * P.kiters;
         const int64_t L = (total + nsm - 1) / nsm;
         const int pieces = static_cast<int>((P.kiters + L - 1) / L) + 1;
         const double t_sk = static_cast<double>(L) + unit_ovh * (1.0 + static_cast<double>(L) / P.kiters) +
-                            static_cast<double>(pieces + 1) * n1 * npad_max * 4.0 /
+                            static_cast<double>(pieces + 1) * n1 * npad_max * P.ncol * 4.0 /
                                 (static_cast<double>(nsm) * a_stage * P.cg);
         if (t_sk < best * 0.97 && ws_cap >= static_cast<size_t>(pieces) * P.ws_per_split) {
             P.sk_len = L;
@@ -285,8 +325,8 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     }
     if ((h->ablate & 8u) && (P.grid & 1)) P.grid += 1;  // cluster-of-2 ablation needs an even grid
     if (getenv("SK_DEBUG_PLAN"))  // tuning diagnostics
-        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d a=%d y=%d o=%d split=%d sk_len=%lld kiters=%d mblk=%d grid=%d smem=%zu\n",
-                static_cast<long long>(n1), static_cast<long long>(k), P.cg, P.cl, P.nacc, P.a_stages, P.y_stages,
+        fprintf(stderr, "[sketch plan] n1=%lld k=%lld cg=%d cl=%d nacc=%d ncol=%d a=%d y=%d o=%d split=%d sk_len=%lld kiters=%d mblk=%d grid=%d smem=%zu\n",
+                static_cast<long long>(n1), static_cast<long long>(k), P.cg, P.cl, P.nacc, P.ncol, P.a_stages, P.y_stages,
                 P.o_stages, P.split, static_cast<long long>(P.sk_len), P.kiters, P.num_mblk, P.grid, P.smem);
     return P;
 }
@@ -379,15 +419,16 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
     const int kshift = static_cast<int>(k0 & 124);
     const int roff = static_cast<int>(k0 & 3);
     const SketchPlan P = plan_sketch(h, m, k, kshift, rs ? ~size_t(0) : ws_bytes, rs ? rs->split : 0);
-    if (rs && (P.npass != 1 || P.split != rs->split))
+    if (rs && (P.npass != 1 || P.split != rs->split || P.ncol != 1))
         return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256 and split <= K iterations");
     CUtensorMap map;
     sk_status_t st = make_map_2d(&map, A, m, k, lda, 32, 128);
     if (st != SK_SUCCESS) return st;
     for (int pass = 0; pass < P.npass; ++pass) {
         sk::SketchGemmParams p{};
-        const int c0 = 256 * pass;
-        p.r_valid = static_cast<int32_t>(std::min<int64_t>(h->r - c0, P.npad[pass]));
+        const int c0 = 256 * P.ncol * pass;
+        const int pass_cols = P.ncol * P.npad[pass];  // output columns of this pass (and partial row length)
+        p.r_valid = static_cast<int32_t>(std::min<int64_t>(h->r - c0, pass_cols));
         p.npad = P.npad[pass];
         p.c0 = c0;
         p.k0a = k0 - kshift;
@@ -421,8 +462,8 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
             p.part_stride = 0;
         } else if (P.split > 1 || P.sk_len > 0) {
             p.out = static_cast<float*>(ws);
-            p.ldo = p.npad;
-            p.part_stride = m * static_cast<int64_t>(p.npad);
+            p.ldo = pass_cols;
+            p.part_stride = m * static_cast<int64_t>(pass_cols);
         } else {
             p.out = B + c0;
             p.ldo = ldb;
@@ -432,18 +473,18 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
         {
             LaunchScope ls(h, SK_PHASE_SKETCH_GEMM, stream);
             e = sk::launch_sketch_gemm(map, p, P.cg, P.nacc, h->dist, h->mode,
-                                       h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream, P.cl);
+                                       h->omega_transform == SK_OMEGA_FAST, P.grid, P.smem, stream, P.cl, P.ncol);
         }
         if (e != cudaSuccess) return cuda_fail(e, "sketch_gemm launch");
         if (P.sk_len > 0 && !rs) {
             LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, stream);
-            e = sk::launch_streamk_reduce(static_cast<const float*>(ws), p.part_stride, p.n1, p.r_valid, p.npad,
+            e = sk::launch_streamk_reduce(static_cast<const float*>(ws), p.part_stride, p.n1, p.r_valid, pass_cols,
                                           B + c0, ldb, P.rows_per_unit, P.kiters, P.sk_len, stream);
             if (e != cudaSuccess) return cuda_fail(e, "streamk_reduce launch");
         } else if (P.split > 1 && !rs) {
             LaunchScope ls(h, SK_PHASE_SPLITK_REDUCE, stream);
             e = sk::launch_splitk_reduce(static_cast<const float*>(ws), p.part_stride, P.split,
-                                         p.n1, p.r_valid, p.npad, B + c0, ldb, stream);
+                                         p.n1, p.r_valid, pass_cols, B + c0, ldb, stream);
             if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce launch");
         }
     }
@@ -674,7 +715,7 @@ sk_status_t sketch_set_trace(sk_sketch_t h, uint64_t* dev_buf, int32_t stages) {
 sk_status_t sketch_workspace_size(sk_sketch_t h, int64_t n1, size_t* bytes) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
     if (!bytes || n1 < 0) return fail(SK_ERR_INVALID_VALUE, "bad workspace query");
-    *bytes = std::max(sketch_ws_bytes(h, n1, h->n2), core_ws_bytes(h, std::max<int64_t>(n1, 1)));
+    *bytes = std::max(sketch_ws_bytes(h, std::max<int64_t>(n1, 1), h->n2), core_ws_bytes(h, std::max<int64_t>(n1, 1)));
     return SK_SUCCESS;
 }
 

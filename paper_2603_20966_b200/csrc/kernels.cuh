@@ -93,8 +93,8 @@ struct LaunchCfg {
 // Host-side launchers (return cudaError_t of the launch).
 cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg,
                                int nacc, int dist, int mode, bool fast, int grid, size_t smem,
-                               cudaStream_t s, int cl = 1);
-int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem);
+                               cudaStream_t s, int cl = 1, int ncol = 1);
+int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem, int ncol = 1);
 size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_stages, bool xa,
                               bool olo, int ks, int nsubo, int y_stages);
 int sketch_gemm_max_smem();

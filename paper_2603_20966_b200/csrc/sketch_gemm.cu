@@ -90,6 +90,24 @@ struct WorkIter {
     }
 };
 
+// Epilogue stores / adds of B rows (strong .gpu-scope operations, so a thread's store and later
+// adds to one address stay in program order in the coherence order: a fixed fp32 summation order).
+__device__ __forceinline__ void st_relaxed_v4(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.relaxed.gpu.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed(float* p, uint32_t a) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(__uint_as_float(a)),
+                 "f"(__uint_as_float(b)), "f"(__uint_as_float(c)), "f"(__uint_as_float(d))
+                 : "memory");
+}
+__device__ __forceinline__ void red_add(float* p, uint32_t a) {
+    asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(__uint_as_float(a)) : "memory");
+}
+
 constexpr uint32_t kATileBytes = 128 * 32 * 4;  // one 128-row x 32-fp32 TMA box
 constexpr int kMaxStages = 8;
 
@@ -133,11 +151,16 @@ __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stag
 // (pair 1-q, half h); each generates half of the slice's rows and a copier thread bulk-copies that
 // half into the partner's stage (completing on the partner's full_o), so every generated Omega
 // element feeds 1024 rows of A.  The partner pair's MMA commit multicasts "stage free" (pfree).
-template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1>
+// NCOL = 2 (with CG = 2, NACC = 1): ONE 128-row A tile per CTA against TWO N = npad Omega column
+// blocks (columns c0 .. c0 + 2 npad), two MMAs per K step into the two halves of TMEM -- a single
+// pass over A for r <= 512 (c4); with CL = 8 (16-CTA clusters) every generated Omega element still
+// feeds 2048 rows of A.
+template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1, int NCOL = 1>
 __global__ void __launch_bounds__(threads_for(MODE), 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
     static_assert(CL == 1 || CG == 2, "Omega sharing between pairs needs CTA pairs");
-    static_assert(CL >= 1 && CL <= 4, "1 to 4 CTA pairs per cluster");
+    static_assert(CL >= 1 && CL <= 8, "1 to 8 CTA pairs per cluster");
+    static_assert(NCOL == 1 || (NCOL == 2 && NACC == 1 && CG == 2), "two column blocks: one A tile per CTA pair half");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -155,7 +178,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     constexpr int kRngW = rng_warps(MODE);                 // Omega producer warps
     constexpr int kRngThreads = kRngW * 32;
     constexpr int kCvtWarps = cvt_warps(MODE);             // bf16 converter warps
-    const int npad_loc = p.npad / CG;  // Omega columns generated / held by this CTA
+    const int nh = p.npad / CG;        // Omega columns of one N block held by this CTA
+    const int npad_loc = NCOL * nh;    // rows of this CTA's Omega tile (all its N blocks)
     const uint32_t osub = static_cast<uint32_t>(npad_loc) * 128u;  // bytes of one Omega sub-tile
     const SmemLayout L = make_layout(NACC, npad_loc, p.a_stages, p.o_stages, ALO, OLO, KS, NSUBO, BF ? p.y_stages : 0);
     uint8_t* sA = smem + L.a_off;
@@ -187,7 +211,7 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     const int group = static_cast<int>(blockIdx.x) / (CG * CL);      // worker = pair (or cluster)
     const int ngroups = static_cast<int>(gridDim.x) / (CG * CL);
     uint32_t tmem_cols = 32;
-    while (tmem_cols < static_cast<uint32_t>(NACC * p.npad)) tmem_cols <<= 1;
+    while (tmem_cols < static_cast<uint32_t>(NACC * NCOL * p.npad)) tmem_cols <<= 1;
 
     if (warp == 0 && lane == 0) {
         // full_a: one expect_tx arrival; with CG = 2 (tf32) the leader's barrier counts the bytes of
@@ -244,20 +268,22 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         float* out = p.out + ((p.split > 1 || p.sk_len > 0) ? static_cast<int64_t>(s) * p.part_stride : 0);
         const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
-        for (int a = 0; a < NACC; ++a) {
+        for (int ac = 0; ac < NACC * NCOL; ++ac) {
+            const int a = ac / NCOL, h = ac % NCOL;
             const int row = mb * rows_per_unit + pair_row0 + a * 128 * CG + static_cast<int>(crank) * 128 +
                             static_cast<int>(q) * 32 + static_cast<int>(lane);
-            float* orow = out + static_cast<int64_t>(row) * p.ldo;
+            float* orow = out + static_cast<int64_t>(row) * p.ldo + h * p.npad;
+            const int rv = p.r_valid - h * p.npad;  // valid columns of this block
             if (p.rs_ndst > 0 && row < p.n1) {
                 // fused reduce-scatter: the row's partial goes straight to its owner's slot
                 // (NVLink store into the peer's receive buffer), no local B / split partial
                 const int64_t piece = row / p.rs_piece;
                 orow = p.rs_dst[piece] + (static_cast<int64_t>(p.rs_slot) * p.split + s) * p.rs_slot_elems +
-                       (row - piece * p.rs_piece) * p.ldo;
+                       (row - piece * p.rs_piece) * p.ldo + h * p.npad;
             }
 #pragma unroll 1
             for (int cc = 0; cc < p.npad; cc += 32) {
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(a * p.npad + cc);
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + static_cast<uint32_t>(ac * p.npad + cc);
                 uint32_t v[32];
                 if (cc + 32 <= p.npad) {
                     tmem_ld_32x32b_x32(taddr, v);
@@ -269,23 +295,27 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 }
                 tmem_ld_wait();
                 if (row < p.n1) {
-                    if (vec_ok && cc + 32 <= p.r_valid) {
+                    if (!first) {
+                        // later chunks: fire-and-forget fp32 RN adds at L2 (REDG.ADD.F32), so the drain
+                        // never waits on a load; one thread owns each element and its adds are
+                        // ordered by program order (same address), so the sum order is fixed
+                        if (vec_ok && cc + 32 <= rv) {
 #pragma unroll
-                        for (int i = 0; i < 32; i += 4) {
-                            float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                                   __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-                            float4* dst = reinterpret_cast<float4*>(orow + cc + i);
-                            if (!first) {
-                                const float4 b = *dst;
-                                o.x = b.x + o.x; o.y = b.y + o.y; o.z = b.z + o.z; o.w = b.w + o.w;
-                            }
-                            *dst = o;
+                            for (int i = 0; i < 32; i += 4)
+                                red_add_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (cc + i < rv) red_add(orow + cc + i, v[i]);
                         }
+                    } else if (vec_ok && cc + 32 <= rv) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4)
+                            st_relaxed_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
-                            if (cc + i < p.r_valid)
-                                orow[cc + i] = first ? __uint_as_float(v[i]) : orow[cc + i] + __uint_as_float(v[i]);
+                            if (cc + i < rv) st_relaxed(orow + cc + i, v[i]);
                     }
                 }
             }
@@ -393,12 +423,13 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
 #pragma unroll
                     for (int k8 = 0; k8 < ((p.ablate & 4u) ? 0 : KMMA); ++k8) {
                         const int sub = k8 >> 2, kk = k8 & 3;  // 32-K sub-tile, 8-K step inside it
-                        const uint64_t bdesc = sw128_desc(o_base + L.ohi_off + sub * osub + kk * 32, 16, 1024);
 #pragma unroll
-                        for (int a = 0; a < NACC; ++a) {
+                        for (int ac = 0; ac < NACC * NCOL; ++ac) {
+                            const int a = ac / NCOL, h = ac % NCOL;  // A tile, Omega column block
+                            const uint64_t bdesc = sw128_desc(o_base + L.ohi_off + sub * osub + h * nh * 128 + kk * 32, 16, 1024);
                             const uint64_t adesc = sw128_desc(a_base + (a * NBOX + sub) * kATileBytes + kk * 32, 16, 1024);
                             uint32_t acc = (ci > 0 || k8 > 0) ? 1u : 0u;
-                            const uint32_t d = tmem_base + a * p.npad;
+                            const uint32_t d = tmem_base + ac * p.npad;
                             if constexpr (X3) {
                                 // small terms first: A_lo * Omega_hi, A_hi * Omega_lo, then A_hi * Omega_hi
                                 const uint64_t alo = sw128_desc(a_base + (NACC + a) * kATileBytes + k8 * 32, 16, 1024);
@@ -507,7 +538,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         const int nthr = split_sub ? kHalfThreads : kRngThreads;
         const int n_start = tt % gen_rows, j_start = tt / gen_rows;
         const int tq = nthr / gen_rows, tr = nthr % gen_rows;
-        const int c0_loc = p.c0 + static_cast<int>(crank) * npad_loc + gen_row0;
+        // this CTA's tile row n is Omega column c0 + (n / nh) npad + crank nh + n % nh; a share lies
+        // inside one column block (the planner's cluster sizes divide the blocks)
+        const int gen_h = gen_row0 / nh;
+        const int c0_loc = p.c0 + gen_h * p.npad + static_cast<int>(crank) * nh + (gen_row0 - gen_h * nh);
         uint32_t so = 0, po = 0, nd = 0, ntr = 0;
         const uint32_t lo_off = L.olo_off - L.ohi_off;
         WorkIter wi(p, group);
@@ -715,23 +749,83 @@ size_t sketch_gemm_smem_bytes(int cg, int nacc, int npad, int a_stages, int o_st
 
 int sketch_gemm_max_smem() { return 227 * 1024; }
 
-// Clusters of `cluster` CTAs of this kernel that can be co-resident (GPC packing strands SMs for
-// clusters of 4).  Returns 0 if the query fails.
-int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem) {
+// The kernel instantiation for a launch configuration (nullptr if not built).  Instantiated: CTA
+// pairs with 2 accumulators and clusters of 2, 3 or 4 pairs (Omega sharing, Gaussian / uniform) or
+// none; the column-pair variant (NCOL = 2, one accumulator) with clusters of 4 or 8 pairs; single
+// CTAs and pairs without sharing for small shapes.
+template <int CG, int NACC, int DIST, int CL, int NCOL>
+static const void* pick_mode(int mode, bool fast) {
+    if (mode == kTF32) {
+        if constexpr (DIST == kGaussian)
+            if (fast) return reinterpret_cast<const void*>(sketch_gemm_kernel<CG, NACC, DIST, kTF32, true, CL, NCOL>);
+        return reinterpret_cast<const void*>(sketch_gemm_kernel<CG, NACC, DIST, kTF32, false, CL, NCOL>);
+    }
+    if (mode == kBF16) {
+        if constexpr (DIST == kGaussian)
+            if (fast) return reinterpret_cast<const void*>(sketch_gemm_kernel<CG, NACC, DIST, kBF16, true, CL, NCOL>);
+        return reinterpret_cast<const void*>(sketch_gemm_kernel<CG, NACC, DIST, kBF16, false, CL, NCOL>);
+    }
+    if constexpr (NCOL == 1)
+        if (mode == kTF32x3) return reinterpret_cast<const void*>(sketch_gemm_kernel<CG, NACC, DIST, kTF32x3, false, CL, NCOL>);
+    return nullptr;
+}
+
+template <int CG, int NACC, int CL, int NCOL>
+static const void* pick_dist(int dist, int mode, bool fast) {
+    if (dist == kGaussian) return pick_mode<CG, NACC, kGaussian, CL, NCOL>(mode, fast);
+    if constexpr (NCOL == 1)
+        if (dist == kRademacher) return pick_mode<CG, NACC, kRademacher, CL, NCOL>(mode, fast);
+    if (dist == kUniform) return pick_mode<CG, NACC, kUniform, CL, NCOL>(mode, fast);
+    return nullptr;
+}
+
+static const void* pick_kernel(int cg, int nacc, int dist, int mode, bool fast, int cl, int ncol) {
+    if (ncol == 2) {
+        if (cg != 2 || nacc != 1 || dist == kRademacher) return nullptr;
+        if (cl == 8) return pick_dist<2, 1, 8, 2>(dist, mode, fast);
+        if (cl == 4) return pick_dist<2, 1, 4, 2>(dist, mode, fast);
+        return nullptr;
+    }
+    if (ncol != 1) return nullptr;
+    if (cl == 4 && cg == 2 && nacc == 2) return pick_dist<2, 2, 4, 1>(dist, mode, fast);
+    if (cl == 3 && cg == 2 && nacc == 2) return pick_dist<2, 2, 3, 1>(dist, mode, fast);
+    if (cl == 2 && cg == 2 && nacc == 2) return pick_dist<2, 2, 2, 1>(dist, mode, fast);
+    if (cl == 2 && cg == 2 && nacc == 1) return pick_dist<2, 1, 2, 1>(dist, mode, fast);
+    if (cl != 1) return nullptr;
+    if (cg == 1 && nacc == 1) return pick_dist<1, 1, 1, 1>(dist, mode, fast);
+    if (cg == 1 && nacc == 2) return pick_dist<1, 2, 1, 1>(dist, mode, fast);
+    if (cg == 2 && nacc == 1) return pick_dist<2, 1, 1, 1>(dist, mode, fast);
+    if (cg == 2 && nacc == 2) return pick_dist<2, 2, 1, 1>(dist, mode, fast);
+    return nullptr;
+}
+
+// Function attributes of an instantiation, once per (device, function): the opt-in smem limit (only
+// ever raised) and, for clusters of more than 8 CTAs, the non-portable cluster size.
+static cudaError_t prepare_kernel(const void* fn, size_t smem, int cluster) {
+    if (cudaError_t e = raise_smem_limit(fn, smem)) return e;
+    if (cluster > 8) return cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return cudaSuccess;
+}
+
+// Clusters of cg * cl CTAs of this kernel that can be co-resident (GPC packing strands SMs for
+// large clusters).  Returns 0 if the query fails or the configuration is not built.
+int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, int cl, size_t smem, int ncol) {
     // per process, keyed by (device, kernel instantiation, smem); guarded: handles may be used from
     // several threads at once (sketch.h)
     static std::mutex mu;
-    static std::map<std::tuple<int, int, int, int, int, int, int, size_t>, int> cache;
+    static std::map<std::tuple<int, const void*, size_t>, int> cache;
+    const void* fn = pick_kernel(cg, nacc, dist, mode, fast, cl, ncol);
+    if (!fn) return 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_tuple(dev, cg, nacc, dist, mode, fast ? 1 : 0, cl, smem);
+    const auto key = std::make_tuple(dev, fn, smem);
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(cg * cl * 64);
+    cfg.gridDim = dim3(cg * cl * 16);
     cfg.blockDim = dim3(threads_for(mode));
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
@@ -742,86 +836,34 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    const void* fn = nullptr;
-#define SK_FN(M, F, C) fn = reinterpret_cast<const void*>(sketch_gemm_kernel<2, 2, kGaussian, M, F, C>)
-    if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 2) {
-        if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 2); else SK_FN(kTF32, false, 2); }
-        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 2); else SK_FN(kBF16, false, 2); }
-        else SK_FN(kTF32x3, false, 2);
-    } else if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 3) {
-        if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 3); else SK_FN(kTF32, false, 3); }
-        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 3); else SK_FN(kBF16, false, 3); }
-        else SK_FN(kTF32x3, false, 3);
-    } else if (cg == 2 && nacc == 2 && dist == kGaussian && cl == 4) {
-        if (mode == kTF32) { if (fast) SK_FN(kTF32, true, 4); else SK_FN(kTF32, false, 4); }
-        else if (mode == kBF16) { if (fast) SK_FN(kBF16, true, 4); else SK_FN(kBF16, false, 4); }
-        else SK_FN(kTF32x3, false, 4);
-    }
-#undef SK_FN
-    if (!fn) return 0;
-    if (raise_smem_limit(fn, smem) != cudaSuccess) return 0;
-    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) return 0;
+    if (prepare_kernel(fn, smem, cg * cl) != cudaSuccess) { cudaGetLastError(); return 0; }
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) { cudaGetLastError(); return 0; }
     std::lock_guard<std::mutex> g(mu);
     cache[key] = n;
     return n;
 }
 
-template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL>
-static cudaError_t launch_one(const CUtensorMap& tmA, const SketchGemmParams& p, int grid,
-                              size_t smem, cudaStream_t s) {
-    auto kern = sketch_gemm_kernel<CG, NACC, DIST, MODE, FAST, CL>;
-    if (cudaError_t e = raise_smem_limit(reinterpret_cast<const void*>(kern), smem)) return e;
+cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg, int nacc,
+                               int dist, int mode, bool fast, int grid, size_t smem,
+                               cudaStream_t s, int cl, int ncol) {
+    const void* fn = pick_kernel(cg, nacc, dist, mode, fast, cl, ncol);
+    if (!fn) return cudaErrorNotSupported;
+    if (cudaError_t e = prepare_kernel(fn, smem, cg * cl)) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads_for(MODE));
+    cfg.blockDim = dim3(threads_for(mode));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     // ablation bit 3: launch single-CTA tiles as clusters of 2 (isolates cluster placement effects)
-    attr[0].val.clusterDim.x = (CG == 1 && (p.ablate & 8u)) ? 2 : CG * CL;
+    attr[0].val.clusterDim.x = (cg == 1 && (p.ablate & 8u)) ? 2 : cg * cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, tmA, p);
-}
-
-template <int CG, int NACC, int DIST, int CL = 1>
-static cudaError_t dispatch_mode(const CUtensorMap& tmA, const SketchGemmParams& p, int mode,
-                                 bool fast, int grid, size_t smem, cudaStream_t s) {
-    if (mode == kTF32) {
-        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kTF32, true, CL>(tmA, p, grid, smem, s);
-        return launch_one<CG, NACC, DIST, kTF32, false, CL>(tmA, p, grid, smem, s);
-    }
-    if (mode == kTF32x3) return launch_one<CG, NACC, DIST, kTF32x3, false, CL>(tmA, p, grid, smem, s);
-    if (mode == kBF16) {
-        if (DIST == kGaussian && fast) return launch_one<CG, NACC, DIST, kBF16, true, CL>(tmA, p, grid, smem, s);
-        return launch_one<CG, NACC, DIST, kBF16, false, CL>(tmA, p, grid, smem, s);
-    }
-    return cudaErrorNotSupported;
-}
-
-template <int CG, int NACC, int CL = 1>
-static cudaError_t dispatch_dist(const CUtensorMap& tmA, const SketchGemmParams& p, int dist,
-                                 int mode, bool fast, int grid, size_t smem, cudaStream_t s) {
-    if (dist == kGaussian) return dispatch_mode<CG, NACC, kGaussian, CL>(tmA, p, mode, fast, grid, smem, s);
-    if (dist == kRademacher) return dispatch_mode<CG, NACC, kRademacher, CL>(tmA, p, mode, fast, grid, smem, s);
-    return dispatch_mode<CG, NACC, kUniform, CL>(tmA, p, mode, fast, grid, smem, s);
-}
-
-cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p, int cg, int nacc,
-                               int dist, int mode, bool fast, int grid, size_t smem,
-                               cudaStream_t s, int cl) {
-    if (cl == 4 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 4>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cl == 3 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 3>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cl == 2 && cg == 2 && nacc == 2) return dispatch_dist<2, 2, 2>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cl == 2 && cg == 2 && nacc == 1) return dispatch_dist<2, 1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cg == 1 && nacc == 1) return dispatch_dist<1, 1>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cg == 1 && nacc == 2) return dispatch_dist<1, 2>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cg == 2 && nacc == 1) return dispatch_dist<2, 1>(tmA, p, dist, mode, fast, grid, smem, s);
-    if (cg == 2 && nacc == 2) return dispatch_dist<2, 2>(tmA, p, dist, mode, fast, grid, smem, s);
-    return cudaErrorNotSupported;
+    void* args[] = {const_cast<CUtensorMap*>(&tmA), const_cast<SketchGemmParams*>(&p)};
+    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace sk

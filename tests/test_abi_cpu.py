@@ -48,6 +48,12 @@ def test_host_validation_without_gpu():
             assert lib.sketch_set_cta_group(h, cg) == 1
         n = ctypes.c_size_t()
         assert lib.sketch_workspace_size(h, 5000, ctypes.byref(n)) == 0
+        # degenerate sizes plan without faulting (empty A, one row), in every mode
+        for mode in (0, 1, 2):
+            assert lib.sketch_set_mode(h, mode) == 0
+            for n1 in (0, 1, 7, 129, 5000, 2048):
+                assert lib.sketch_workspace_size(h, n1, ctypes.byref(n)) == 0
+        assert lib.sketch_workspace_size(h, -1, ctypes.byref(n)) == 1
         # shape mismatch is reported before any device work
         st = lib.sketch_apply(h, None, 10, 999, 999, None, 64, None, 0, None)
         assert lib.sketch_status_string(st) == b"SK_ERR_SHAPE_MISMATCH"

@@ -576,3 +576,32 @@ def test_c4_shape_sampled_rows(mode, omega):
     Bref = oracle.sketch(SEED, "gaussian", Ad[rows].cpu().numpy(), r)
     assert _relF(B[rows].cpu().numpy(), Bref) <= TOL[mode]
     del Ad
+
+
+@pytest.mark.parametrize("split", [1, 3])
+def test_tf32x3_long_k_without_split(split):
+    """tf32x3's fp32 accuracy must not depend on the split: K = 20,000 in ONE unit (split_k = 1) runs
+    20 TMEM accumulation chunks of <= 1024 K, each promoted into the output in fp32 RN (DESIGN §7.5);
+    the truncating TMEM accumulation alone would give ~1.4e-4 here."""
+    sk = _sk()
+    n1, n2, r = 640, 20000, 64
+    A = synth.uniform(13, n1, n2)
+    s = sk.Sketch(SEED, "gaussian", n2, r, mode="tf32x3", split_k=split)
+    B = s.apply(_dev(A)).cpu().numpy()
+    assert _relF(B, oracle.sketch(SEED, "gaussian", A, r)) <= 1e-5
+
+
+@pytest.mark.parametrize("n1", [700, 1100, 2048])
+@pytest.mark.parametrize("mode,omega", [("bf16", "fast"), ("tf32", "accurate"), ("bf16", "accurate")])
+def test_wide_r_single_pass(n1, mode, omega):
+    """256 < r <= 512 in ONE pass over A (two N = 256 Omega column blocks per CTA; clusters of 4 pairs
+    for n1 <= 1024, of 8 pairs = 16 CTAs above): Gaussian and uniform Omega against the oracle."""
+    sk = _sk()
+    n2, r = 3000, 400
+    A = synth.uniform(14, n1, n2)
+    for dist in ("gaussian", "uniform"):
+        if dist == "uniform" and omega == "fast":
+            continue
+        s = sk.Sketch(SEED, dist, n2, r, mode=mode, omega=omega)
+        B = s.apply(_dev(A)).cpu().numpy()
+        assert _relF(B, oracle.sketch(SEED, dist, A, r)) <= TOL[mode], dist
