@@ -72,6 +72,24 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# The JSON line is the only thing on stdout: everything else written to file descriptor 1 while
+# the bench runs -- NCCL's version banner, library prints -- is sent to stderr.
+_JSON_FD = None
+
+
+def _stdout_to_stderr():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    sys.stdout.flush()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(obj) + "\n").encode())
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -242,7 +260,7 @@ def run_reference(args, W, wl_name):
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------------------- f4 ablation
@@ -327,7 +345,7 @@ def relaunch_under_torchrun(n: int) -> None:
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
     log("[bench] launching " + " ".join(cmd[1:]))
-    sys.exit(subprocess.call(cmd))
+    sys.exit(subprocess.call(cmd, stdout=_JSON_FD if _JSON_FD is not None else None))
 
 
 def main():
@@ -711,11 +729,12 @@ def main():
             result["e2e"] = {"error": repr(e)}
 
     if rank == 0:
-        print(json.dumps(result), flush=True)
+        emit(result)
     if world > 1:
         tdist.barrier(device_ids=[local_rank])
     tdist.destroy_process_group()
 
 
 if __name__ == "__main__":
+    _stdout_to_stderr()
     main()

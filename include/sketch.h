@@ -88,15 +88,20 @@ sk_status_t sketch_set_omega_transform(sk_sketch_t h, sk_omega_transform_t t);
 sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k);
 
 /* Tuning / ablation override of the sketch GEMM's CTA grouping: 0 = automatic (CTA pairs with
- * tcgen05 cta_group::2 for n1 > 256; in bf16 mode, clusters of two pairs sharing the generated
- * Gaussian Omega slices for n1 >= 2048), 1 = single-CTA tiles, 2 = CTA pairs without sharing,
+ * tcgen05 cta_group::2 for n1 > 256; Gaussian Omega in tf32 / bf16: clusters of 4 pairs sharing the
+ * generated slices for n1 >= 2048, of 3 pairs for bf16 with SK_OMEGA_FAST at n1 >= 6144; for
+ * 256 < r <= 512 (or r a multiple of 512) with Gaussian / uniform Omega in tf32 / bf16, one pass per
+ * 512 columns with two N = 256 column blocks per CTA in clusters of 8 pairs = 16 CTAs, or 4 pairs
+ * where 16-CTA clusters do not fit), 1 = single-CTA tiles, 2 = CTA pairs without sharing,
  * 4 = clusters of 2 pairs sharing Omega whenever the shape allows it (any mode), 6 = clusters of 3
- * pairs (6 CTAs; the automatic choice for bf16 with SK_OMEGA_FAST at n1 >= 6144), 8 = clusters of 4
- * pairs (8 CTAs) sharing Omega.  Any other value: SK_ERR_INVALID_VALUE. */
+ * pairs (6 CTAs), 8 = clusters of 4 pairs (8 CTAs) sharing Omega.  A non-zero override also keeps
+ * 256-column passes.  Any other value: SK_ERR_INVALID_VALUE. */
 sk_status_t sketch_set_cta_group(sk_sketch_t h, int32_t cg);
 
-/* Core GEMM implementation: 0 = tcgen05 (default for r <= 256, tf32 operands), 1 = fp32 SIMT
- * (used automatically for r > 256 or a B whose rows are not 16-byte aligned). */
+/* Core GEMM implementation: 0 = tcgen05 (default, any r: blocks of up to 256 x 256 of C with tf32
+ * operands in the tf32 / bf16 modes; 128 x 128 blocks with 3xTF32 operands (hi + lo splits of Omega
+ * and B, <= 1024 rows per TMEM accumulation) in tf32x3), 1 = fp32 SIMT (used automatically for a B
+ * whose rows are not 16-byte aligned). */
 sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt);
 
 /* Performance ablation for measurements only (results are WRONG while set): bit 0 skips the
@@ -147,6 +152,17 @@ sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslot
  * elems % 4 == 0.  Stream-ordered; the caller orders it after all ranks' writes (device barrier).
  * Errors: SK_ERR_INVALID_VALUE, SK_ERR_SHAPE_MISMATCH, SK_ERR_ALIGNMENT. */
 sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, void* stream);
+
+/* NVLS reduction (the AllReduce of C, and the reduce-scatter of
+ * partial B, done inside the NVSwitch): out[i] = sum over the ranks of a multicast
+ * group of their copies of element i, for i < elems, read through the group's multicast mapping
+ * `mc_src` (multimem.ld_reduce.add.f32, round-to-nearest); if `mc_out` (a multicast address) is
+ * non-NULL the sums are also stored to every rank's copy there.  mc_src / mc_out: device multicast
+ * virtual addresses (e.g. torch symmetric memory's multicast_ptr + byte offset); out: local device
+ * buffer or NULL.  The caller orders the ranks' writes of the inputs before the call (a barrier).
+ * elems % 4 == 0, all pointers 16-byte aligned.  Stream-ordered.  Errors: SK_ERR_INVALID_VALUE,
+ * SK_ERR_SHAPE_MISMATCH, SK_ERR_ALIGNMENT, SK_ERR_CUDA (e.g. no multicast support). */
+sk_status_t sketch_multimem_sum(const float* mc_src, int64_t elems, float* out, float* mc_out, void* stream);
 
 /* Pack of the Redist variant's All-to-All ("unpack" step PAPER.md:1536): for column
  * bounds cb[0] = 0 < cb[1] < ... < cb[nblk] <= ldb, writes block j = B[0:rows, cb[j]:cb[j+1]]

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation", "sketch_set_trace",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
-    "sketch_rs_split", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers", "sketch_pack_cols",
+    "sketch_rs_split", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers", "sketch_multimem_sum", "sketch_pack_cols",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
@@ -87,6 +87,7 @@ def load_library(build_if_missing: bool = True):
                                               i32, vp]
         lib.sketch_reduce_slots.argtypes = [vp, vp, i32, i64, i64, vp, i64, vp]
         lib.sketch_sum_peers.argtypes = [ctypes.POINTER(vp), i32, i64, vp, vp]
+        lib.sketch_multimem_sum.argtypes = [vp, i64, vp, vp, vp]
         lib.sketch_pack_cols.argtypes = [vp, i64, i64, ctypes.POINTER(i64), i32, vp, vp]
         lib.sketch_set_trace.argtypes = [vp, vp, i32]
         lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
@@ -417,6 +418,16 @@ def sum_peers(src_ptrs, elems: int, out, stream=None):
     arr = (ctypes.c_void_p * len(src_ptrs))(*[ctypes.c_void_p(int(x)) for x in src_ptrs])
     _check(load_library().sketch_sum_peers(arr, ctypes.c_int32(len(src_ptrs)), ctypes.c_int64(elems),
                                            ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+    return out
+
+
+def multimem_sum(mc_src: int, elems: int, out=None, mc_out: int = 0, stream=None):
+    """out[:elems] = sum over the multicast group's ranks of element i at the multicast address mc_src
+    (NVLS in-switch reduction; see sketch_multimem_sum); optionally broadcast to mc_out."""
+    _require_cuda(out)
+    _check(load_library().sketch_multimem_sum(ctypes.c_void_p(int(mc_src)), ctypes.c_int64(elems),
+                                              ctypes.c_void_p(out.data_ptr() if out is not None else 0),
+                                              ctypes.c_void_p(int(mc_out)), _stream_ptr(stream)))
     return out
 
 

@@ -815,6 +815,15 @@ sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, 
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "peer sum launch");
 }
 
+sk_status_t sketch_multimem_sum(const float* mc_src, int64_t elems, float* out, float* mc_out, void* stream) {
+    if (!mc_src || elems < 0 || (!out && !mc_out)) return fail(SK_ERR_INVALID_VALUE, "bad multicast reduction arguments");
+    if (elems % 4 != 0) return fail(SK_ERR_SHAPE_MISMATCH, "elems must be a multiple of 4");
+    if (!aligned16(mc_src) || (out && !aligned16(out)) || (mc_out && !aligned16(mc_out)))
+        return fail(SK_ERR_ALIGNMENT, "multicast reduction needs 16-byte aligned buffers");
+    cudaError_t e = sk::launch_multimem_sum(mc_src, elems, out, mc_out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "multimem sum launch");
+}
+
 sk_status_t sketch_pack_cols(const float* B, int64_t rows, int64_t ldb, const int64_t* cb, int32_t nblk,
                              float* out, void* stream) {
     if (!cb || nblk < 1 || nblk > 64 || rows < 0) return fail(SK_ERR_INVALID_VALUE, "bad column-pack arguments");
@@ -1050,7 +1059,8 @@ const char* sketch_status_string(sk_status_t st) {
 const char* sketch_last_error(void) { return g_last_error.c_str(); }
 
 const char* sketch_build_info(void) {
-    return "libsketch sm_100a (tcgen05 tf32 sketch GEMM, SIMT core GEMM v1)";
+    return "libsketch sm_100a (tcgen05 sketch GEMM: tf32 / bf16 / 3xTF32, fused Philox4x32-10 Omega tiles; "
+           "tcgen05 core GEMM with regenerated Omega; fixed-order reductions)";
 }
 
 }  // extern "C"

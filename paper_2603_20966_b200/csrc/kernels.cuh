@@ -102,6 +102,7 @@ cudaError_t raise_smem_limit(const void* fn, size_t smem);
 
 cudaError_t launch_pack_cols(const float* B, int64_t rows, int64_t ldb, const int64_t* cb, int32_t nblk,
                              float* out, cudaStream_t s);
+cudaError_t launch_multimem_sum(const float* mc_src, int64_t elems, float* out, float* mc_out, cudaStream_t s);
 cudaError_t launch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, cudaStream_t s);
 cudaError_t launch_streamk_reduce(const float* part, int64_t part_stride, int32_t n1, int32_t r_valid,
                                   int32_t ldp, float* out, int64_t ldo, int32_t rows_per_unit, int32_t kiters,

@@ -333,6 +333,10 @@ class DistSketch:
         self.fused_ar = bool(fused_ar) and r % 4 == 0
         self._ar = None
         self.fallbacks = []  # (what, error) of symmetric-memory setups that fell back to NCCL
+        # f1 over NVLS: symmetric-memory reductions inside the NVSwitch when the buffers have a
+        # multicast mapping (SK_NVLS=0: NVLink peer reads instead)
+        self.nvls = os.environ.get("SK_NVLS", "1") != "0"
+        self.reduce_path = None  # "nvls" / "peer" once a symmetric-memory reduction ran
 
     # ------------------------------------------------------------------ symmetric memory setup
     def _symm(self, comm, shape, device, what):
@@ -396,10 +400,10 @@ class DistSketch:
     def _apply_peer_rs(self, A_blk, rows, per, c0):
         """Alg. 1 line 415 over symmetric memory: B-bar (rows padded to p2 * per) is written into this
         rank's slot (two slots alternating per call), one device barrier over the row group, then the
-        owner of piece j sums rows [j per, (j+1) per) of the p2 slots over NVLink in rank order.
+        owner of piece j sums rows [j per, (j+1) per) of the p2 slots -- inside the NVSwitch (NVLS)
+        when the slots have a multicast mapping, else over NVLink in rank order.
         Returns None (and switches to NCCL on every rank) if symmetric memory cannot be set up."""
         import torch
-        from . import sum_peers
         p2, r = self.layout.p2, self.r
         key = (rows, per)
         if self._rsp is None or self._rsp["key"] != key:
@@ -418,9 +422,21 @@ class DistSketch:
         a, b = self.b_piece_rows()
         piece = torch.empty((per, r), dtype=torch.float32, device=A_blk.device)
         off = (k * p2 * per + self.j * per) * r * 4
-        sum_peers([p + off for p in sb.ptrs], per * r, piece)
+        self._reduce(sb, off, per * r, piece)
         self.comm_bytes += 4 * per * r * (p2 - 1)
         return piece[: b - a], (a, b)
+
+    def _reduce(self, sb, off: int, elems: int, out):
+        """out[:elems] = sum over the group of the symmetric buffers at byte offset `off`: inside the
+        NVSwitch through the multicast mapping (NVLS, `sketch_multimem_sum`) when the group has one,
+        else NVLink peer reads in rank order (`sketch_sum_peers`)."""
+        from . import multimem_sum, sum_peers
+        if self.nvls and sb.multicast_ptr and elems % 4 == 0:
+            multimem_sum(sb.multicast_ptr + off, elems, out)
+            self.reduce_path = "nvls"
+        else:
+            sum_peers([p + off for p in sb.ptrs], elems, out)
+            self.reduce_path = "peer"
 
     def _apply_fused_rs(self, A_blk, rows, per, c0):
         """Alg. 1 line 415 with the reduce-scatter fused into the GEMM epilogue: every
@@ -507,9 +523,9 @@ class DistSketch:
     def _core_fused_allreduce(self, Bp, a):
         """AllReduce of the r x r core partials without NCCL: each rank's core GEMM
         writes its partial into its own symmetric-memory slot (two slots, alternating per call), one
-        device barrier, then every rank sums all ranks' slots over NVLink in rank order."""
+        device barrier, then every rank sums all ranks' slots: in the NVSwitch (NVLS multimem
+        ld_reduce) when the slots have a multicast mapping, else over NVLink in rank order."""
         import torch
-        from . import sum_peers
         r = self.r
         if self._ar is None:
             sb = self._symm(self.comm, (2, r * r), Bp.device, "fused AllReduce")
@@ -524,7 +540,7 @@ class DistSketch:
         self.local.core_block(Bp, a, out=sb.tensor[k].view(r, r))
         sb.barrier()  # every rank's partial is in its slot k
         C = torch.empty((r, r), dtype=torch.float32, device=Bp.device)
-        sum_peers([p + k * r * r * 4 for p in sb.ptrs], r * r, C)
+        self._reduce(sb, k * r * r * 4, r * r, C)
         self.comm_bytes += r * r * 4
         return C
 
