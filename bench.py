@@ -578,6 +578,7 @@ def main():
         "comm": {"variant": args.variant if (W["nystrom"] and world > 1) else None,
                  "reduce_scatter": ds.rs_mode,
                  "fused_allreduce": bool(ds.fused_ar and world > 1),
+                 "symmetric_reduce_path": ds.reduce_path,  # "nvls" (in-switch multimem) / "peer" (NVLink reads)
                  "predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"],
                                                                      args.variant if world > 1 else "noredist"),
                  "measured_bytes_per_rank": comm_bytes},

@@ -133,6 +133,11 @@ def test_fused_allreduce_of_core_matches_nccl_and_oracle():
         assert np.array_equal(out[True].astype(np.float64), Cref)
 
 
+def _has_multicast(ds):
+    ar = getattr(ds, "_ar", None)
+    return bool(ar and ar["sb"].multicast_ptr)
+
+
 def _worker_layouts(rank, world, port, n, r, q):
     """Every Nystrom variant on real GPUs over NCCL + symmetric memory: No-Redist on the row-block and
     (for 4 ranks) 2 x 2 grids with the peer-read reduce-scatter and the fused AllReduce, and Redist."""
@@ -162,7 +167,7 @@ def _worker_layouts(rank, world, port, n, r, q):
                     Bp, (a, b), C = ds.nystrom_core_redist(Ablk) if variant == "redist" else ds.nystrom_core(Ablk)
                 torch.cuda.synchronize()
                 out[(spec, variant)] = (a, b, Bp.cpu().numpy(), C.cpu().numpy(), ds.rs_mode, ds.fused_ar,
-                                        list(ds.fallbacks))
+                                        list(ds.fallbacks), ds.reduce_path, _has_multicast(ds))
         q.put((rank, out))
     finally:
         tdist.destroy_process_group()
@@ -194,11 +199,13 @@ def test_all_variants_nccl_match_oracle(world):
     A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
     Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
     for rank, out in res:
-        for (spec, variant), (a, b, Bp, C, rs_mode, fused_ar, fallbacks) in out.items():
+        for (spec, variant), (a, b, Bp, C, rs_mode, fused_ar, fallbacks, path, mc) in out.items():
             assert np.array_equal(Bp.astype(np.float64), Bref[a:b]), (spec, variant)
             assert np.array_equal(C.astype(np.float64), Cref), (spec, variant)
             assert not fallbacks, fallbacks
             if variant == "noredist":
                 assert fused_ar
+                # the in-switch (NVLS) reduction runs whenever the symmetric buffers have a multicast mapping
+                assert path == ("nvls" if mc else "peer"), (path, mc)
                 if spec != "row":
                     assert rs_mode == "peer"
