@@ -158,11 +158,9 @@ class TorchComm:
         grp = self.group if self.group is not None else self.tdist.group.WORLD
         buf = symm_mem.empty(shape, dtype=dtype, device=device)
         hdl = symm_mem.rendezvous(buf, grp.group_name)
-        mc = 0
-        try:
-            if hdl.has_multicast_support():
-                mc = int(hdl.multicast_ptr)
-        except Exception:  # pragma: no cover - older torch
+        try:  # non-zero when the group's buffers have a multicast (NVLS) mapping
+            mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+        except Exception:  # pragma: no cover - no multicast object on this box
             mc = 0
         return SymmBuf(buf, [int(x) for x in hdl.buffer_ptrs], lambda: hdl.barrier(channel=0), mc)
 

@@ -9,8 +9,8 @@ torch.cuda.set_device(rank)
 dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
 buf = symm_mem.empty((1024,), dtype=torch.float32, device="cuda")
 hdl = symm_mem.rendezvous(buf, dist.group.WORLD.group_name)
-mc = hdl.multicast_ptr if hdl.has_multicast_support() else 0
-print(f"rank {rank}: has_multicast_support={hdl.has_multicast_support()} multicast_ptr={mc:#x}", flush=True)
+mc = int(getattr(hdl, "multicast_ptr", 0) or 0)
+print(f"rank {rank}: multicast_ptr={mc:#x}", flush=True)
 if mc:
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
