@@ -90,15 +90,48 @@ def emit(obj):
     os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(obj) + "\n").encode())
 
 
+SPEC = {"hbm": 7700.0, "bf16": 2250.0, "tf32": 1100.0}  # nominal B200 (B200_PROFILING.md table): context only
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as f:
             p = json.load(f)
-        return dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
-                    bf16_sus=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
-                    source="MEASURED_PEAKS.json (measured)")
-    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="B200_PROFILING.md fallback")
+        pk = dict(hbm=float(p["hbm_gbs"]), bf16=float(p["bf16_tflops"]),
+                  bf16_sus=float(p.get("bf16_tflops_sustained", p["bf16_tflops"])),
+                  source="MEASURED_PEAKS.json (measured)")
+    else:
+        pk = dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, source="B200_PROFILING.md fallback")
+    # TF32: cuBLAS TF32 8192^3 measured on this pool (tools/measure_tf32_peak.py), else bf16 x nominal ratio
+    tp = os.path.join(ROOT, "profiles", "tf32_peak.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            pk["tf32"] = float(json.load(f)["tf32_tflops"])
+        pk["tf32_source"] = "profiles/tf32_peak.json (cuBLAS TF32 8192^3, measured)"
+    else:
+        pk["tf32"] = pk["bf16"] * NOMINAL_TF32_OVER_BF16
+        pk["tf32_source"] = "bf16 measured x 1.1/2.25 nominal"
+    return pk
+
+
+def roofline(mode, kern_bytes, kern_flops, kern_s, peaks):
+    """Roofline of the sketch kernel for one step's launches: the binding resource is whichever of HBM
+    (algorithmic bytes / measured copy bandwidth) and the tensor pipe (flops / the measured peak of the
+    mode's MMA: bf16; tf32; tf32x3 = tf32 / 3, three MMAs per product) takes longer at its peak."""
+    tc_peak = {"bf16": peaks["bf16"], "tf32": peaks["tf32"], "tf32x3": peaks["tf32"] / 3.0}[mode]
+    tc_spec = {"bf16": SPEC["bf16"], "tf32": SPEC["tf32"], "tf32x3": SPEC["tf32"] / 3.0}[mode]
+    gbs = kern_bytes / kern_s / 1e9
+    tfs = kern_flops / kern_s / 1e12
+    if kern_bytes / (peaks["hbm"] * 1e9) >= kern_flops / (tc_peak * 1e12):
+        roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm"], "unit": "GB/s", "frac": gbs / peaks["hbm"],
+                "spec_peak": SPEC["hbm"], "spec_frac": gbs / SPEC["hbm"]}
+    else:
+        roof = {"bound": "tensor", "achieved": tfs, "peak": tc_peak, "unit": "TFLOP/s", "frac": tfs / tc_peak,
+                "spec_peak": tc_spec, "spec_frac": tfs / tc_spec}
+    roof.update({"hbm_frac": gbs / peaks["hbm"], "tensor_frac": tfs / tc_peak,
+                 "peak_source": peaks["source"] + ("; " + peaks["tf32_source"] if mode != "bf16" else ", bf16 burst")})
+    return roof
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -532,23 +565,11 @@ def main():
     avg_s = (gemm_ms / max(gemm_launches, 1)) * 1e-3
     passes = max(1, gemm_launches // max(args.steps, 1))
     avg_s_step = avg_s * passes  # all column passes of one step
-    tc_peak = {"tf32": peaks["bf16"] * NOMINAL_TF32_OVER_BF16, "tf32x3": peaks["bf16"] * NOMINAL_TF32_OVER_BF16 / 3.0,
-               "bf16": peaks["bf16"]}[args.mode]
-    t_hbm = kern_bytes / (peaks["hbm"] * 1e9)
-    t_tc = kern_flops / (tc_peak * 1e12)
-    if t_hbm >= t_tc:
-        ach = kern_bytes / avg_s_step / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"]}
-    else:
-        ach = kern_flops / avg_s_step / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak}
+    roof = roofline(args.mode, kern_bytes, kern_flops, avg_s_step, peaks)
     roof.update({
         "kernel": f"sketch_gemm_kernel (fused Philox/Box-Muller Omega tiles + tcgen05 {args.mode})",
         "launches_timed": gemm_launches, "avg_launch_ms": avg_s * 1e3,
         "share_of_step": (gemm_ms / max(t_ms, 1e-9)),
-        "hbm_frac": (kern_bytes / avg_s_step / 1e9) / peaks["hbm"],
-        "tensor_frac": (kern_flops / avg_s_step / 1e12) / tc_peak,
-        "peak_source": peaks["source"] + (", tf32 = bf16 burst x 1.1/2.25 nominal" if args.mode != "bf16" else ", bf16 burst"),
         "traffic": None,
     })
     prof_path = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{args.mode}_{args.omega}.json")
@@ -598,23 +619,32 @@ def main():
                 def step2():
                     return ds2.nystrom_core(A) if W["nystrom"] else ds2.apply(A)
 
-                for _ in range(2):
+                for _ in range(3):
                     step2()
                 torch.cuda.synchronize()
                 barrier()
+                reps = max(3, args.steps // 2)
+                loc2.set_profiling(True)
+                loc2.profile_read()
                 g0 = torch.cuda.Event(enable_timing=True)
                 g1 = torch.cuda.Event(enable_timing=True)
                 g0.record(stream)
-                for _ in range(max(3, args.steps // 2)):
+                for _ in range(reps):
                     step2()
                 g1.record(stream)
                 torch.cuda.synchronize()
-                t2 = torch.tensor([g0.elapsed_time(g1) / max(3, args.steps // 2)], dtype=torch.float64,
+                ph2 = loc2.profile_read()
+                loc2.set_profiling(False)
+                t2 = torch.tensor([g0.elapsed_time(g1) / reps], dtype=torch.float64,
                                   device=dev if world > 1 else "cpu")
                 if world > 1:
                     tdist.all_reduce(t2, op=tdist.ReduceOp.MAX)
                 t2 = float(t2.item())
-                others[f"{mode}/{omega}"] = {"ms_per_step": t2, "value": a_bytes_total / (t2 * 1e-3) / 1e9}
+                sk_s = ph2["sketch_gemm"][0] / reps * 1e-3  # sketch kernel time per step (all its launches)
+                others[f"{mode}/{omega}"] = {
+                    "ms_per_step": t2, "value": a_bytes_total / (t2 * 1e-3) / 1e9,
+                    "phases_ms_per_step": {k: v[0] / reps for k, v in ph2.items() if v[1]},
+                    "roofline": roofline(mode, kern_bytes, kern_flops, sk_s, peaks) if sk_s > 0 else None}
                 del loc2, ds2
             except Exception as e:  # pragma: no cover
                 others[f"{mode}/{omega}"] = {"error": repr(e)}
@@ -661,11 +691,17 @@ def main():
                 if t >= 10.0 or nrows >= min(A.shape[0], 16384):
                     break
                 nrows = int(min(min(A.shape[0], 16384), max(2 * nrows, nrows * 12.0 / max(t, 1e-3))))
+            # the paper's phase split (genOmegaTime / dgemm1Time): the oracle's
+            # materialisation of Omega alone, the rest of the call is the fp64 GEMM
+            t0 = time.perf_counter()
+            oracle.omega(SEED_OMEGA, W["dist"], 0, n2, 0, r)
+            t_om = time.perf_counter() - t0
             result["cpu_baseline"] = {
                 "value": nrows * n2 * 4 / t / 1e9, "unit": "GB/s", "cores": oracle.num_threads(),
                 "kind": "oracle",
                 "sample": f"B = A Omega for rows 0..{nrows - 1} of {n1} (full K={n2}, r={r}), fp64, "
                           f"Omega materialised once; {t:.1f} s",
+                "phases_s": {"gen_omega": t_om, "gemm": max(t - t_om, 0.0)},
             }
         except Exception as e:  # pragma: no cover
             result["cpu_baseline"] = {"error": repr(e)}

@@ -811,7 +811,11 @@ sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, 
         if (!src[j] || !aligned16(src[j])) return fail(SK_ERR_ALIGNMENT, "sources must be 16-byte aligned");
     if (!aligned16(out)) return fail(SK_ERR_ALIGNMENT, "out must be 16-byte aligned");
     if (elems == 0) return SK_SUCCESS;
-    cudaError_t e = sk::launch_sum_peers(src, n, elems, out, static_cast<cudaStream_t>(stream));
+    cudaError_t e;
+    {
+        LaunchScope ls(nullptr, 0, static_cast<cudaStream_t>(stream));
+        e = sk::launch_sum_peers(src, n, elems, out, static_cast<cudaStream_t>(stream));
+    }
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "peer sum launch");
 }
 
@@ -820,7 +824,11 @@ sk_status_t sketch_multimem_sum(const float* mc_src, int64_t elems, float* out, 
     if (elems % 4 != 0) return fail(SK_ERR_SHAPE_MISMATCH, "elems must be a multiple of 4");
     if (!aligned16(mc_src) || (out && !aligned16(out)) || (mc_out && !aligned16(mc_out)))
         return fail(SK_ERR_ALIGNMENT, "multicast reduction needs 16-byte aligned buffers");
-    cudaError_t e = sk::launch_multimem_sum(mc_src, elems, out, mc_out, static_cast<cudaStream_t>(stream));
+    cudaError_t e;
+    {
+        LaunchScope ls(nullptr, 0, static_cast<cudaStream_t>(stream));
+        e = sk::launch_multimem_sum(mc_src, elems, out, mc_out, static_cast<cudaStream_t>(stream));
+    }
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "multimem sum launch");
 }
 
@@ -833,7 +841,11 @@ sk_status_t sketch_pack_cols(const float* B, int64_t rows, int64_t ldb, const in
     if (cb[nblk] > ldb) return fail(SK_ERR_SHAPE_MISMATCH, "cb[nblk] > ldb");
     if (rows == 0 || cb[nblk] == 0) return SK_SUCCESS;
     if (!B || !out) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
-    cudaError_t e = sk::launch_pack_cols(B, rows, ldb, cb, nblk, out, static_cast<cudaStream_t>(stream));
+    cudaError_t e;
+    {
+        LaunchScope ls(nullptr, 0, static_cast<cudaStream_t>(stream));
+        e = sk::launch_pack_cols(B, rows, ldb, cb, nblk, out, static_cast<cudaStream_t>(stream));
+    }
     return e == cudaSuccess ? SK_SUCCESS : cuda_fail(e, "pack_cols launch");
 }
 

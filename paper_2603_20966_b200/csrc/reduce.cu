@@ -150,27 +150,42 @@ cudaError_t launch_sum_peers(const float* const* src, int32_t n, int64_t elems, 
 // NVLS (NVLink SHARP): out[i] = sum over the multicast group's ranks of their copies of mc_src[i],
 // reduced inside the NVSwitch (multimem.ld_reduce, fp32 RN) -- one read per element per rank instead
 // of P peer reads; optionally broadcast back through the multicast mapping (multimem.st).
+__device__ __forceinline__ float4 multimem_ld_sum(const float* mc) {
+    float4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(mc)
+                 : "memory");
+    return v;
+}
+
+// 4 independent in-switch loads in flight per thread (each crosses NVLink to every rank's copy)
 __global__ void multimem_sum_kernel(const float* __restrict__ mc_src, int64_t n4, float* __restrict__ out,
                                     float* __restrict__ mc_out) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        float a, b, c, d;
-        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
-                     : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
-                     : "l"(mc_src + 4 * i)
-                     : "memory");
-        if (out) reinterpret_cast<float4*>(out)[i] = make_float4(a, b, c, d);
-        if (mc_out)
-            asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_out + 4 * i), "f"(a),
-                         "f"(b), "f"(c), "f"(d)
-                         : "memory");
+    constexpr int kU = 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += stride * kU) {
+        float4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (i0 + u * stride < n4) v[u] = multimem_ld_sum(mc_src + 4 * (i0 + u * stride));
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i >= n4) break;
+            if (out) reinterpret_cast<float4*>(out)[i] = v[u];
+            if (mc_out)
+                asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_out + 4 * i),
+                             "f"(v[u].x), "f"(v[u].y), "f"(v[u].z), "f"(v[u].w)
+                             : "memory");
+        }
     }
 }
 
 cudaError_t launch_multimem_sum(const float* mc_src, int64_t elems, float* out, float* mc_out, cudaStream_t s) {
     const int64_t n4 = elems / 4;
     if (n4 <= 0) return cudaSuccess;
-    const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 4));
+    const int blocks = static_cast<int>(std::min<int64_t>((n4 + 1023) / 1024, 148 * 2));
     multimem_sum_kernel<<<blocks, 256, 0, s>>>(mc_src, n4, out, mc_out);
     return cudaGetLastError();
 }
