@@ -6,6 +6,7 @@ vectors, independently computed worked values, closed forms, library routines
 names the plausible mistake it is there to catch.
 """
 import math
+import os
 import struct
 
 import numpy as np
@@ -300,3 +301,17 @@ def test_nystrom_error_decreases_with_rank():
         At = B @ np.linalg.pinv(C, rcond=1e-12, hermitian=True) @ B.T
         errs.append(np.linalg.norm(At - A) / np.linalg.norm(A))
     assert errs[0] > errs[1] > errs[2]
+
+
+def test_worked_values_regenerate_from_independent_generator():
+    """tests/golden/omega_worked.txt is reproduced by its committed generator (an independent pure-Python
+    Philox4x32-10 + O1 mapping that imports neither oracle/ nor the package)."""
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    gen = os.path.join(here, "golden", "gen_omega_worked.py")
+    src = open(gen).read()
+    assert "import oracle" not in src and "paper_2603_20966_b200" not in src
+    out = subprocess.run([sys.executable, gen], capture_output=True, text=True, check=True).stdout
+    with open(os.path.join(here, "golden", "omega_worked.txt")) as f:
+        assert out == f.read()
