@@ -404,8 +404,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="replay each step as one CUDA graph (auto: on for 1 GPU when A < 1 GB, i.e. the "
-                         "launch-latency-bound c1); per-phase times then come from a profiled eager pass")
+                    help="replay the steps as CUDA graphs (auto: on for N > 1, and for 1 GPU when A < 1 GB, i.e. "
+                         "the launch-latency-bound c1); per-phase times then come from a profiled eager pass")
     ap.add_argument("--nccl-ar", action="store_true",
                     help="AllReduce C with NCCL instead of the default fused NVLink peer-read sum (f1, symmetric memory)")
     ap.add_argument("--rs", default="peer", choices=["nccl", "peer", "epilogue"],
@@ -503,12 +503,70 @@ def main():
     barrier()
     per_step = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
     launches = sk.launch_count() - launches0
+    comm_bytes = ds.comm_bytes / args.steps  # python-side accounting of the eager timed steps
     phases = local.profile_read()
     local.set_profiling(False)
     t_ms = e0.elapsed_time(e1)
-    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and 4.0 * n1 * n2 < 1e9)
+    use_graph = args.graph == "on" or (args.graph == "auto" and (world > 1 or 4.0 * n1 * n2 < 1e9))
     graph_info = None
     eager_ms_step = t_ms / args.steps
+    if use_graph and world > 1:
+        # N > 1: the step (sketch, split-K reduce, symmetric-memory barriers, reduce-scatter / AllReduce
+        # kernels, core GEMM) captured as CUDA graphs and replayed; two steps per graph so the
+        # alternating receive slots keep alternating (plus a one-step graph for an odd K).  All ranks
+        # capture in lockstep and agree on success before replaying.
+        gerr = None
+        try:
+            gs = torch.cuda.Stream()
+            gs.wait_stream(stream)
+            with torch.cuda.stream(gs):
+                for _ in range(2):
+                    out = step()
+            stream.wait_stream(gs)
+            torch.cuda.synchronize()
+            g2 = torch.cuda.CUDAGraph()
+            lc0 = sk.launch_count()
+            with torch.cuda.graph(g2, stream=gs):
+                step()
+                out = step()
+            launches_per_step = (sk.launch_count() - lc0) / 2.0
+            g1 = None
+            if args.steps % 2:
+                g1 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g1, stream=gs):
+                    out = step()
+        except Exception as e:  # pragma: no cover - capture unsupported here
+            gerr = repr(e)
+        okt = torch.tensor([0 if gerr else 1], dtype=torch.int32, device=dev)
+        tdist.all_reduce(okt, op=tdist.ReduceOp.MIN)
+        if int(okt.item()) == 1:
+            for _ in range(max(2, args.warmup // 2)):
+                g2.replay()
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            npair = args.steps // 2
+            pair_ev = [torch.cuda.Event(enable_timing=True) for _ in range(max(npair, 1))]
+            e0.record(stream)
+            h0 = time.perf_counter()
+            for i in range(npair):
+                g2.replay()
+                pair_ev[i].record(stream)
+            if g1 is not None:
+                g1.replay()
+            host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            t_ms = e0.elapsed_time(e1)
+            if npair:
+                per_step = [e0.elapsed_time(pair_ev[0]) / 2.0] + [pair_ev[i - 1].elapsed_time(pair_ev[i]) / 2.0
+                                                                  for i in range(1, npair)]
+            launches = int(round(launches_per_step * args.steps))
+            graph_info = {"replayed": True, "steps_per_graph": 2, "launches_per_step": launches_per_step,
+                          "eager_ms_per_step": eager_ms_step}
+        else:
+            graph_info = {"replayed": False, "error": gerr or "capture failed on another rank"}
     if use_graph and world == 1:
         # the step captured once as a CUDA graph (library launches on the capture stream) and replayed:
         # the eager pass above supplied the per-phase kernel times
@@ -542,7 +600,6 @@ def main():
         graph_info = {"replayed": True, "launches_per_step": launches_per_step,
                       "eager_ms_per_step": eager_ms_step}
     clocks = sampler.stop()
-    comm_bytes = ds.comm_bytes / args.steps
     tmax = torch.tensor([t_ms], dtype=torch.float64, device=dev if world > 1 else "cpu")
     if world > 1:
         tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)

@@ -1,0 +1,9 @@
+# ring-depth sweeps: c4 shape (K = 1e6) and c2 (50000^2), bf16 / fast
+P="python tools/prof_shape.py 2048 1000000 512 bf16 fast gaussian 5"
+Q="python tools/prof_shape.py 50000 50000 256 bf16 fast gaussian 5"
+for cfg in "" "SK_Y_STAGES=3" "SK_Y_STAGES=3 SK_A_STAGES=2" "SK_A_STAGES=4 SK_O_STAGES=3" "SK_A_STAGES=4 SK_Y_STAGES=1 SK_O_STAGES=3" "SK_O_STAGES=3"; do
+  echo "c4 [$cfg]" $(env $cfg SK_DEBUG_PLAN=1 $P 2>&1 | grep -E "plan|GB/s" | sed -e 's/.*a=\([0-9]\) y=\([0-9]\) o=\([0-9]\).*grid=\([0-9]*\).*/a=\1 y=\2 o=\3 grid=\4/' | sort -u | tr '\n' ' ')
+done > gpurun_out/r2m_sweep.txt 2>&1
+for cfg in "" "SK_Y_STAGES=3" "SK_O_STAGES=6" "SK_A_STAGES=4" "SK_A_STAGES=4 SK_O_STAGES=3" "SK_A_STAGES=2 SK_Y_STAGES=3"; do
+  echo "c2 [$cfg]" $(env $cfg SK_DEBUG_PLAN=1 $Q 2>&1 | grep -E "plan|GB/s" | sed -e 's/.*a=\([0-9]\) y=\([0-9]\) o=\([0-9]\).*grid=\([0-9]*\).*/a=\1 y=\2 o=\3 grid=\4/' | sort -u | tr '\n' ' ')
+done >> gpurun_out/r2m_sweep.txt 2>&1

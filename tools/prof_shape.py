@@ -1,5 +1,6 @@
 """B = A Omega on one shape, for ncu / sanitizer runs and quick timings.
-usage: python tools/prof_shape.py N1 N2 R MODE OMEGA DIST [REPS]   (A ~ U[-1/2, 1/2) generated on the GPU)"""
+usage: [CG=0|1|2|4|6|8] python tools/prof_shape.py N1 N2 R MODE OMEGA DIST [REPS]
+(A ~ U[-1/2, 1/2) generated on the GPU; CG = sketch_set_cta_group override)"""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,7 +11,7 @@ n1, n2, r = (int(x) for x in sys.argv[1:4])
 mode, omega, dist = sys.argv[4:7]
 reps = int(sys.argv[7]) if len(sys.argv) > 7 else 3
 A = torch.empty((n1, n2), device="cuda").uniform_(-0.5, 0.5)
-s = sk.Sketch(42, dist, n2, r, mode=mode, omega=omega)
+s = sk.Sketch(42, dist, n2, r, mode=mode, omega=omega, cta_group=int(os.environ.get("CG", "0")))
 B = torch.empty((n1, r), device="cuda")
 s.apply(A, out=B)
 torch.cuda.synchronize()
