@@ -404,8 +404,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="replay the steps as CUDA graphs (auto: on for N > 1, and for 1 GPU when A < 1 GB, i.e. "
-                         "the launch-latency-bound c1); per-phase times then come from a profiled eager pass")
+                    help="replay the timed steps as CUDA graphs (auto = on); the per-phase kernel times then come "
+                         "from the profiled eager pass that precedes them")
     ap.add_argument("--nccl-ar", action="store_true",
                     help="AllReduce C with NCCL instead of the default fused NVLink peer-read sum (f1, symmetric memory)")
     ap.add_argument("--rs", default="peer", choices=["nccl", "peer", "epilogue"],
@@ -507,7 +507,7 @@ def main():
     phases = local.profile_read()
     local.set_profiling(False)
     t_ms = e0.elapsed_time(e1)
-    use_graph = args.graph == "on" or (args.graph == "auto" and (world > 1 or 4.0 * n1 * n2 < 1e9))
+    use_graph = args.graph == "on" or args.graph == "auto"
     graph_info = None
     eager_ms_step = t_ms / args.steps
     if use_graph and world > 1:

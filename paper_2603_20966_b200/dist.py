@@ -335,7 +335,9 @@ class DistSketch:
         # multicast mapping (SK_NVLS=0: NVLink peer reads instead)
         self.nvls = os.environ.get("SK_NVLS", "1") != "0"
         # nystrom_core on 2D / column layouts: core GEMM on the local B-bar beside the B reduce-scatter
-        self.overlap_core = os.environ.get("SK_OVERLAP_CORE", "1") != "0"
+        # (opt-in: at p2 = 2 the doubled core rows cost what the overlap saves -- 1x2 c2 at 2 GPUs:
+        # 1.099 ms with vs 1.085 ms without, r2o)
+        self.overlap_core = os.environ.get("SK_OVERLAP_CORE", "0") == "1"
         self._side_stream = None
         self._overlap_rs = False
         self._last_bbar = None
