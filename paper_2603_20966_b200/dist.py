@@ -334,6 +334,9 @@ class DistSketch:
         # f1 over NVLS: symmetric-memory reductions inside the NVSwitch when the buffers have a
         # multicast mapping (SK_NVLS=0: NVLink peer reads instead)
         self.nvls = os.environ.get("SK_NVLS", "1") != "0"
+        # ... for groups of at least this many ranks (2 ranks: the NVLink peer read is as fast or faster,
+        # r2j / r2p); SK_NVLS_MIN overrides
+        self.nvls_min_ranks = int(os.environ.get("SK_NVLS_MIN", "4"))
         # nystrom_core on 2D / column layouts: core GEMM on the local B-bar beside the B reduce-scatter
         # (opt-in: at p2 = 2 the doubled core rows cost what the overlap saves -- 1x2 c2 at 2 GPUs:
         # 1.099 ms with vs 1.085 ms without, r2o)
@@ -443,7 +446,7 @@ class DistSketch:
         NVSwitch through the multicast mapping (NVLS, `sketch_multimem_sum`) when the group has one,
         else NVLink peer reads in rank order (`sketch_sum_peers`)."""
         from . import multimem_sum, sum_peers
-        if self.nvls and sb.multicast_ptr and elems % 4 == 0:
+        if self.nvls and sb.multicast_ptr and elems % 4 == 0 and len(sb.ptrs) >= self.nvls_min_ranks:
             multimem_sum(sb.multicast_ptr + off, elems, out)
             self.reduce_path = "nvls"
         else:

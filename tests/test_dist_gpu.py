@@ -161,6 +161,7 @@ def _worker_layouts(rank, world, port, n, r, q):
                 local = sk.Sketch(SEED, "rademacher", n, r, mode="tf32")
                 ds = DistSketch(SEED, "rademacher", n, n, r, Layout.parse(spec, world), local=local,
                                 fused_rs="peer", fused_ar=True)
+                ds.nvls_min_ranks = 2  # exercise the in-switch path on every group that has it
                 r0, r1, c0, c1 = ds.a_block_range()
                 Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1])).to(dev)
                 for _ in range(2):
