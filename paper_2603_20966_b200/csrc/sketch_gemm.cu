@@ -310,12 +310,21 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                         }
                     } else if (vec_ok && cc + 32 <= rv) {
 #pragma unroll
-                        for (int i = 0; i < 32; i += 4)
-                            st_relaxed_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        for (int i = 0; i < 32; i += 4) {
+                            if constexpr (X3)  // later chunks add to it: a strong store, ordered before them
+                                st_relaxed_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            else
+                                *reinterpret_cast<float4*>(orow + cc + i) =
+                                    make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                                __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+                        }
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (cc + i < rv) st_relaxed(orow + cc + i, v[i]);
+                        for (int i = 0; i < 32; ++i) {
+                            if (cc + i >= rv) continue;
+                            if constexpr (X3) st_relaxed(orow + cc + i, v[i]);
+                            else orow[cc + i] = __uint_as_float(v[i]);
+                        }
                     }
                 }
             }
@@ -406,8 +415,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             WorkIter wi(p, group);
             int mb, kb, ke, s;
             while (wi.next(p, ngroups, mb, kb, ke, s)) {
+                int ci = 0;  // K iteration inside the accumulation chunk (a counter: no division here)
                 for (int kit = kb; kit < ke; ++kit, ++ntr) {
-                    const int ci = (kit - kb) % kchunk;  // K iteration inside the accumulation chunk
                     if (ci == 0) {  // the epilogue has drained the previous chunk
                         mbar_wait(tmem_empty, (nd & 1) ^ 1);
                         tc_fence_after();
@@ -463,10 +472,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     }
                     if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                     if (++so == static_cast<uint32_t>(p.o_stages)) { so = 0; po ^= 1; }
-                    if (ci == kchunk - 1 || kit + 1 == ke) {  // chunk complete: hand TMEM to the epilogue
+                    if (++ci == kchunk || kit + 1 == ke) {  // chunk complete: hand TMEM to the epilogue
                         if constexpr (CG == 2) mma_commit_pair(tmem_full, pair_mask);
                         else mma_commit(tmem_full);
                         ++nd;
+                        ci = 0;
                     }
                 }
             }
@@ -615,6 +625,8 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
         WorkIter wi(p, group);
         int mb, kb, ke, s;
         while (wi.next(p, ngroups, mb, kb, ke, s)) {
+            int ci = 0;
+            bool first = true;
             for (int kit = kb; kit < ke; ++kit) {
                 if (cw == 0) mbar_wait(&full_a[sa], pa);
                 asm volatile("bar.sync 2, %0;" ::"n"(kCvtWarps * 32) : "memory");
@@ -638,10 +650,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                     else mbar_arrive(&conv[sa]);
                 }
                 if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
-                const int ci = (kit - kb) % kchunk;
-                if (ci == kchunk - 1 || kit + 1 == ke) {
-                    drain(static_cast<uint32_t>(cw), mb, s, kit - kb < kchunk, nd);
+                if (++ci == kchunk || kit + 1 == ke) {
+                    drain(static_cast<uint32_t>(cw), mb, s, first, nd);
                     ++nd;
+                    ci = 0;
+                    first = false;
                 }
             }
         }
