@@ -143,3 +143,15 @@ def test_virtual_overlapped_core_exact(world, spec):
     Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
     res = _run(world, spec, n, n, r, "rademacher", "tf32", A, rs="peer", fused_ar=True, overlap=True, steps=3)
     _check_exact(res, Bref, Cref, n)
+
+
+@pytest.mark.parametrize("world,spec", [(2, "col"), (4, "2x2")])
+def test_virtual_epilogue_rs_tf32x3(world, spec):
+    """tf32x3 with the reduce-scatter fused into the sketch epilogue: the promoted TMEM chunks are
+    stored / added (ordered L2 reductions) straight into the owners' receive slots; exact in the
+    integer regime, and K = 4,000 per rank spans several 1024-K chunks."""
+    n1, n2, r = 900, 8000, 40
+    A = synth.int_matrix(5, n1, n2, -4, 4)
+    Bref = oracle.sketch(SEED, "rademacher", A, r)
+    res = _run(world, spec, n1, n2, r, "rademacher", "tf32x3", A, rs="epilogue")
+    _check_exact(res, Bref, None, n1)
