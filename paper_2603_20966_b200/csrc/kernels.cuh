@@ -33,6 +33,12 @@ struct SketchGemmParams {
     int32_t prefetch;     // K steps of A prefetched into L2 ahead of the TMA loads (0 = off)
     int32_t kchunk;       // > 0 (tf32x3): K iterations per TMEM accumulation; each chunk is drained
                           // and added (fp32 RN) into the unit's output, which accumulates in place
+    int32_t inplace;      // 1: the split / stream-K pieces of an m-block accumulate straight into out
+                          // (= B) in DESCENDING piece order (the top piece stores, each lower piece
+                          // waits for the one above it, then adds): no partials, no reduce kernel
+    int32_t max_pieces;   // inplace: pieces per m-block (flag array stride)
+    int32_t* flags;       // inplace: [m-block][piece][CTA of the cluster] completion flags, zeroed
+                          // before the launch
     int64_t sk_len;       // > 0: stream-K -- worker w runs flattened (m-block, K-iteration) indices
                           // [w sk_len, (w+1) sk_len), cut at m-block boundaries; partial `piece` =
                           // w - first worker touching the m-block (split / kper unused)

@@ -262,10 +262,34 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
     // rows of this CTA's 128-row tiles): tcgen05.ld -> the unit's output row (B, the split / stream-K
     // partial `s`, or a peer's receive slot) -- stored for the first chunk of the unit, added (fp32 RN,
     // same thread every time: a fixed order) for later ones -- then TMEM is handed back to the MMA.
+    // In-place accumulation of the pieces of an m-block (p.inplace): flag of (m-block, piece, this CTA);
+    // the 4 drain warps (128 threads, named barrier 3) wait for the piece above / publish their own.
+    auto piece_flag = [&](int mb, int piece) {
+        return p.flags + (static_cast<int64_t>(mb) * p.max_pieces + piece) * (CG * CL) + crank_cl;
+    };
+    auto wait_piece_above = [&](uint32_t q, int mb, int piece) {
+        if (q == 0 && lane == 0) {
+            const int32_t* f = piece_flag(mb, piece + 1);
+            int32_t v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if (v != 0) break;
+                __nanosleep(100);
+            }
+        }
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+    };
+    auto publish_piece = [&](uint32_t q, int mb, int piece) {
+        asm volatile("bar.sync 3, 128;" ::: "memory");  // every drain thread's stores / adds are issued
+        if (q == 0 && lane == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(piece_flag(mb, piece)), "r"(1) : "memory");
+        }
+    };
     auto drain = [&](uint32_t q, int mb, int s, bool first, uint32_t nd) {
         mbar_wait(tmem_full, nd & 1);
         tc_fence_after();
-        float* out = p.out + ((p.split > 1 || p.sk_len > 0) ? static_cast<int64_t>(s) * p.part_stride : 0);
+        float* out = p.out + ((!p.inplace && (p.split > 1 || p.sk_len > 0)) ? static_cast<int64_t>(s) * p.part_stride : 0);
         const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
         for (int ac = 0; ac < NACC * NCOL; ++ac) {
@@ -606,7 +630,11 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
             }
             if (!X3 && t < 128) {
                 // epilogue: warp (4+q) reads TMEM lanes 32q..32q+31 = rows of this CTA's half
-                drain(static_cast<uint32_t>(t >> 5), mb, s, true, nd);
+                const uint32_t q = static_cast<uint32_t>(t >> 5);
+                const bool top = ke == p.kiters;  // the piece holding the last K iterations stores first
+                if (p.inplace && !top) wait_piece_above(q, mb, s);
+                drain(q, mb, s, !p.inplace || top, nd);
+                if (p.inplace) publish_piece(q, mb, s);
                 ++nd;
             }
         }
@@ -651,7 +679,10 @@ __global__ void __launch_bounds__(threads_for(MODE), 1)
                 }
                 if (++sa == static_cast<uint32_t>(p.a_stages)) { sa = 0; pa ^= 1; }
                 if (++ci == kchunk || kit + 1 == ke) {
-                    drain(static_cast<uint32_t>(cw), mb, s, first, nd);
+                    const bool top = ke == p.kiters;
+                    if (p.inplace && !top && first) wait_piece_above(static_cast<uint32_t>(cw), mb, s);
+                    drain(static_cast<uint32_t>(cw), mb, s, first && (!p.inplace || top), nd);
+                    if (p.inplace && kit + 1 == ke) publish_piece(static_cast<uint32_t>(cw), mb, s);
                     ++nd;
                     ci = 0;
                     first = false;
