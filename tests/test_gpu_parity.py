@@ -605,3 +605,29 @@ def test_wide_r_single_pass(n1, mode, omega):
         s = sk.Sketch(SEED, dist, n2, r, mode=mode, omega=omega)
         B = s.apply(_dev(A)).cpu().numpy()
         assert _relF(B, oracle.sketch(SEED, dist, A, r)) <= TOL[mode], dist
+
+
+@pytest.mark.parametrize("mode,omega", [("bf16", "fast"), ("tf32", "accurate")])
+def test_streamk_inplace_pieces(mode, omega, capfd, monkeypatch):
+    """The 8-GPU per-rank shape of c2 (12,500 x 25,000): stream-K pieces of each m-block accumulated in
+    place into B in descending piece order (no partials, no reduce kernel) -- sampled rows against the
+    oracle, bit-identical reruns, and the same B as the partials + reduce path (SK_INPLACE=0) within
+    fp32 rounding."""
+    sk = _sk()
+    n1, n2, r = 12500, 25000, 256
+    Ad = synth.uniform_device(21, n1, n2)
+    monkeypatch.setenv("SK_DEBUG_PLAN", "1")
+    s = sk.Sketch(SEED, "gaussian", n2, r, mode=mode, omega=omega)
+    B1 = s.apply(Ad)
+    B2 = s.apply(Ad)
+    torch.cuda.synchronize()
+    plan = capfd.readouterr().err
+    if mode == "bf16":  # measured plan at this shape (profiles/r2_share_cluster_sweep.txt): stream-K
+        assert "sk_len=0 " not in [l for l in plan.splitlines() if "sketch plan" in l][-1], plan
+    assert torch.equal(B1, B2)
+    rows = [0, 1, 1535, 1536, 6000, 12287, 12499]
+    Bref = oracle.sketch(SEED, "gaussian", Ad[rows].cpu().numpy(), r)
+    assert _relF(B1[rows].cpu().numpy(), Bref) <= TOL[mode]
+    monkeypatch.setenv("SK_INPLACE", "0")
+    B3 = sk.Sketch(SEED, "gaussian", n2, r, mode=mode, omega=omega).apply(Ad)
+    assert _relF(B1.cpu().numpy(), B3.double().cpu().numpy()) <= 1e-6
