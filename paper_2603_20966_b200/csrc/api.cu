@@ -412,13 +412,27 @@ struct RsTarget {
 
 sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int64_t lda,
                        int64_t k0, float* B, int64_t ldb, void* ws, size_t ws_bytes,
-                       cudaStream_t stream, const RsTarget* rs = nullptr) {
+                       cudaStream_t stream, const RsTarget* rs = nullptr, bool split_rows = true) {
     if (m == 0) return SK_SUCCESS;
     // Omega tile rows start at a 128-aligned global row (+ roff = k0 % 4); the matching A columns
     // start kshift (a multiple of 4) columns left of column 0 and are zero-filled by TMA.
     const int kshift = static_cast<int>(k0 & 124);
     const int roff = static_cast<int>(k0 & 3);
     const SketchPlan P = plan_sketch(h, m, k, kshift, rs ? ~size_t(0) : ws_bytes, rs ? rs->split : 0);
+    // A small ragged remainder of rows (<= 1/4 of a cluster unit) would cost a whole unit of Omega
+    // generation and MMA in the clustered launch (6250 rows = 4.07 units of 1536: 19% waste at the
+    // 8-GPU row share); run the whole units clustered and the remainder as a second, small launch
+    // planned for its own size (same stream, disjoint rows of B).
+    if (split_rows && !rs && P.cl > 1 && getenv("SK_NO_REMAINDER") == nullptr) {
+        const int64_t m_main = (m / P.rows_per_unit) * P.rows_per_unit;
+        const int64_t m_rem = m - m_main;
+        if (m_main > 0 && m_rem > 0 && 4 * m_rem <= P.rows_per_unit) {
+            if (sk_status_t st = apply_impl(h, A, m_main, k, lda, k0, B, ldb, ws, ws_bytes, stream, nullptr, false))
+                return st;
+            return apply_impl(h, A + m_main * lda, m_rem, k, lda, k0, B + m_main * ldb, ldb, ws, ws_bytes, stream,
+                              nullptr, false);
+        }
+    }
     if (rs && (P.npass != 1 || P.split != rs->split || P.ncol != 1))
         return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256 and split <= K iterations");
     CUtensorMap map;

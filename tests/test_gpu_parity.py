@@ -631,3 +631,18 @@ def test_streamk_inplace_pieces(mode, omega, capfd, monkeypatch):
     monkeypatch.setenv("SK_INPLACE", "0")
     B3 = sk.Sketch(SEED, "gaussian", n2, r, mode=mode, omega=omega).apply(Ad)
     assert _relF(B1.cpu().numpy(), B3.double().cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("mode,omega,n1", [("bf16", "fast", 6250), ("tf32", "accurate", 6250), ("bf16", "fast", 2100)])
+def test_ragged_row_remainder_second_launch(mode, omega, n1):
+    """n1 = whole cluster units + a small remainder (6250 = 4 x 1536 + 106; 2100 = 2048 + 52): the whole
+    units run clustered, the remainder as a second launch planned for its own size; every row against
+    the oracle (Gaussian, relF), and bit-exact in the integer regime."""
+    sk = _sk()
+    n2, r = 3000, 256
+    A = synth.uniform(23, n1, n2)
+    B = sk.Sketch(SEED, "gaussian", n2, r, mode=mode, omega=omega).apply(_dev(A)).cpu().numpy()
+    assert _relF(B, oracle.sketch(SEED, "gaussian", A, r)) <= TOL[mode]
+    Ai = synth.int_matrix(24, n1, n2)
+    Bi = sk.Sketch(SEED, "rademacher", n2, r, mode=mode).apply(_dev(Ai)).cpu().numpy()
+    assert np.array_equal(Bi.astype(np.float64), oracle.sketch(SEED, "rademacher", Ai, r))
