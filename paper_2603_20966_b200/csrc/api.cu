@@ -412,27 +412,13 @@ struct RsTarget {
 
 sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int64_t lda,
                        int64_t k0, float* B, int64_t ldb, void* ws, size_t ws_bytes,
-                       cudaStream_t stream, const RsTarget* rs = nullptr, bool split_rows = true) {
+                       cudaStream_t stream, const RsTarget* rs = nullptr) {
     if (m == 0) return SK_SUCCESS;
     // Omega tile rows start at a 128-aligned global row (+ roff = k0 % 4); the matching A columns
     // start kshift (a multiple of 4) columns left of column 0 and are zero-filled by TMA.
     const int kshift = static_cast<int>(k0 & 124);
     const int roff = static_cast<int>(k0 & 3);
     const SketchPlan P = plan_sketch(h, m, k, kshift, rs ? ~size_t(0) : ws_bytes, rs ? rs->split : 0);
-    // A small ragged remainder of rows (<= 1/4 of a cluster unit) would cost a whole unit of Omega
-    // generation and MMA in the clustered launch (6250 rows = 4.07 units of 1536: 19% waste at the
-    // 8-GPU row share); run the whole units clustered and the remainder as a second, small launch
-    // planned for its own size (same stream, disjoint rows of B).
-    if (split_rows && !rs && P.cl > 1 && getenv("SK_NO_REMAINDER") == nullptr) {
-        const int64_t m_main = (m / P.rows_per_unit) * P.rows_per_unit;
-        const int64_t m_rem = m - m_main;
-        if (m_main > 0 && m_rem > 0 && 4 * m_rem <= P.rows_per_unit) {
-            if (sk_status_t st = apply_impl(h, A, m_main, k, lda, k0, B, ldb, ws, ws_bytes, stream, nullptr, false))
-                return st;
-            return apply_impl(h, A + m_main * lda, m_rem, k, lda, k0, B + m_main * ldb, ldb, ws, ws_bytes, stream,
-                              nullptr, false);
-        }
-    }
     if (rs && (P.npass != 1 || P.split != rs->split || P.ncol != 1))
         return fail(SK_ERR_UNSUPPORTED, "fused reduce-scatter needs r <= 256 and split <= K iterations");
     CUtensorMap map;
@@ -441,16 +427,16 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
     // In-place accumulation of split / stream-K pieces (no partials, no reduce kernel) whenever no
     // piece can wait on a unit its own worker runs later: stream-K (a lower piece is the LAST unit of
     // its worker, the piece above the FIRST unit of the next worker), or split-K whose pieces of one
-    // m-block fall in the same wave (one wave, or a wave width that is a multiple of the split) and
-    // are few: simultaneous pieces publish one after another, so a long chain (c4: 7 pieces of one
-    // m-block, 2.75 -> 2.80 ms) costs more than the reduce it saves (c2: 1.951 -> 1.933 ms,
-    // 25000 x 25000: 0.525 -> 0.505 ms; r2w).
+    // m-block fall in the same wave (one wave, or a wave width that is a multiple of the split); and
+    // only for <= 4 pieces per m-block: pieces that finish together publish one after another, so a
+    // long chain costs more than the reduce it saves (c4: 7 pieces, 2.75 -> 2.80 ms; 106 rows with 132
+    // stream-K pieces: 0.67 ms; c2: 1.951 -> 1.933 ms and 25000 x 25000: 0.525 -> 0.505 ms; r2w, r2y).
     const int ngroups = P.grid / (P.cg * P.cl);
     const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
     const bool pieces = P.split > 1 || P.sk_len > 0;
     const char* ip_env = getenv("SK_INPLACE");  // tuning: SK_INPLACE=0 keeps partials + reduce
     const bool inplace = !rs && pieces && !(ip_env && atoi(ip_env) == 0) &&
-                         (P.sk_len > 0 || (P.split <= 4 && (units <= ngroups || ngroups % P.split == 0)));
+                         P.split <= 4 && (P.sk_len > 0 || units <= ngroups || ngroups % P.split == 0);
     const size_t inplace_flag_bytes =
         static_cast<size_t>(std::max(P.num_mblk, 1)) * P.split * P.cg * P.cl * sizeof(int32_t);
     if (inplace && (!ws || ws_bytes < inplace_flag_bytes))

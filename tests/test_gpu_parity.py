@@ -634,10 +634,10 @@ def test_streamk_inplace_pieces(mode, omega, capfd, monkeypatch):
 
 
 @pytest.mark.parametrize("mode,omega,n1", [("bf16", "fast", 6250), ("tf32", "accurate", 6250), ("bf16", "fast", 2100)])
-def test_ragged_row_remainder_second_launch(mode, omega, n1):
-    """n1 = whole cluster units + a small remainder (6250 = 4 x 1536 + 106; 2100 = 2048 + 52): the whole
-    units run clustered, the remainder as a second launch planned for its own size; every row against
-    the oracle (Gaussian, relF), and bit-exact in the integer regime."""
+def test_ragged_row_remainder(mode, omega, n1):
+    """n1 = whole cluster units + a small remainder (6250 = 4 x 1536 + 106; 2100 = 2048 + 52): the last
+    cluster unit is mostly empty rows (TMA zero fill, rows >= n1 never stored); every row against the
+    oracle (Gaussian, relF), and bit-exact in the integer regime."""
     sk = _sk()
     n2, r = 3000, 256
     A = synth.uniform(23, n1, n2)
