@@ -435,8 +435,10 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
     const int64_t units = static_cast<int64_t>(P.num_mblk) * P.split;
     const bool pieces = P.split > 1 || P.sk_len > 0;
     const char* ip_env = getenv("SK_INPLACE");  // tuning: SK_INPLACE=0 keeps partials + reduce
+    const char* ipm_env = getenv("SK_INPLACE_MAX");  // tuning: most pieces per m-block accumulated in place
+    const int inplace_max = ipm_env ? atoi(ipm_env) : 4;
     const bool inplace = !rs && pieces && !(ip_env && atoi(ip_env) == 0) &&
-                         P.split <= 4 && (P.sk_len > 0 || units <= ngroups || ngroups % P.split == 0);
+                         P.split <= inplace_max && (P.sk_len > 0 || units <= ngroups || ngroups % P.split == 0);
     const size_t inplace_flag_bytes =
         static_cast<size_t>(std::max(P.num_mblk, 1)) * P.split * P.cg * P.cl * sizeof(int32_t);
     if (inplace && (!ws || ws_bytes < inplace_flag_bytes))
