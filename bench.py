@@ -411,6 +411,9 @@ def main():
     ap.add_argument("--omega-ablation", action="store_true",
                     help="f4: also time B = A*Omega with Omega materialised in HBM (+ all-gathered over NCCL "
                          "when N > 1) and a cuBLAS GEMM, against the fused in-kernel regeneration")
+    ap.add_argument("--no-balance", action="store_true",
+                    help="row-block grids: plain balanced row split instead of whole cluster units per rank with "
+                         "the ragged tail rows split by columns")
     ap.add_argument("--no-other-modes", action="store_true",
                     help="skip timing the other precision modes / transforms after the main line")
     args = ap.parse_args()
@@ -451,21 +454,28 @@ def main():
     peaks = load_peaks()
 
     local = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=args.mode, omega=args.omega, split_k=args.split_k)
+    # row-block grids cut at whole units of the library's plan (the ragged tail split by columns)
+    unit = 0
+    if layout.p2 == 1 and world > 1 and not args.no_balance:
+        unit = local.plan_info(-(-n1 // world), n2)["rows_per_unit"]
     ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.rs,
-                    fused_ar=not args.nccl_ar)
+                    fused_ar=not args.nccl_ar, balance_unit=unit)
     r0, r1, c0, c1 = ds.a_block_range()
     t_gen = time.perf_counter()
     A = make_A_block(W, args.workload, r0, r1, c0, c1, dev)
+    tail = ds.tail_block_range()
+    A_tail = make_A_block(W, args.workload, *tail, dev) if tail is not None else None
     torch.cuda.synchronize()
-    log(f"[bench] rank {rank}: A block {tuple(A.shape)} generated in {time.perf_counter() - t_gen:.1f}s")
+    log(f"[bench] rank {rank}: A block {tuple(A.shape)}" + (f" + tail block {tuple(A_tail.shape)}" if tail else "") +
+        f" generated in {time.perf_counter() - t_gen:.1f}s")
     stream = torch.cuda.current_stream()
 
     def step():
         if W["nystrom"] and args.variant == "redist" and world > 1:
-            return ds.nystrom_core_redist(A)
+            return ds.nystrom_core_redist(A, A_tail)
         if W["nystrom"]:
-            return ds.nystrom_core(A)
-        Bp, rows = ds.apply(A)
+            return ds.nystrom_core(A, A_tail)
+        Bp, rows = ds.apply(A, A_tail)
         return Bp, rows, None
 
     def barrier():
@@ -640,6 +650,8 @@ def main():
         "vs_baseline": None, "dtype": args.mode, "data": "synthetic (seeded, generated in HBM)",
         "config": {"workload": W["desc"], "n1": n1, "n2": n2, "r": r, "dist": W["dist"], "mode": args.mode,
                    "omega_transform": args.omega, "layout": f"{layout.p1}x{layout.p2}",
+                   "row_split": (f"{ds.tail['M']} rows per rank (whole units of {unit}) + the {ds.tail['R']}-row tail "
+                                 f"split by columns, reduced onto rank {world - 1}" if ds.tail else "balanced"),
                    "layout_rule": ("paper sec. 4.3 grid selection: Case 1 (P x 1) since P <= n1 (PAPER.md:438-440)"
                                    if args.layout == "auto" and W["nystrom"] else args.layout),
                    "l2": "inputs larger than L2 (A = %.1f GB)" % (a_bytes_total / 1e9) if a_bytes_total > 126e6
@@ -657,7 +669,8 @@ def main():
                  "fused_allreduce": bool(ds.fused_ar and world > 1),
                  "symmetric_reduce_path": ds.reduce_path,  # "nvls" (in-switch multimem) / "peer" (NVLink reads)
                  "predicted_bytes_per_rank": predicted_bytes_per_rank(n1, r, layout, W["nystrom"],
-                                                                     args.variant if world > 1 else "noredist"),
+                                                                     args.variant if world > 1 else "noredist",
+                                                                     tail_rows=ds.tail["R"] if ds.tail else 0),
                  "measured_bytes_per_rank": comm_bytes},
     }
 
@@ -715,7 +728,7 @@ def main():
         try:
             import oracle
             Bp, (a, b), C = out
-            rows = sorted(set(int(x) for x in np.linspace(a, b - 1, 24)))
+            rows = sorted(set(int(x) for x in np.linspace(a, min(b, a + A.shape[0]) - 1, 24)))  # bulk block rows
             # the exact device rows of A (and, for row-block layouts, all of K) go to the oracle
             A_rows = A[[x - r0 for x in rows]].cpu().numpy() if (c0, c1) == (0, n2) else None
             if A_rows is not None:
@@ -771,10 +784,15 @@ def main():
         try:
             Ah = torch.empty(A.shape, dtype=torch.float32, pin_memory=True)
             Ah.copy_(A)
-            rows_b = r1 - r0
+            pa, pb = ds.b_piece_rows()
+            rows_b = pb - pa
             Bh = torch.empty((rows_b, r), dtype=torch.float32, pin_memory=True)
             Ch = torch.empty((r, r), dtype=torch.float32, pin_memory=True)
-            host_row_layout = (c0, c1) == (0, n2)
+            host_row_layout = (c0, c1) == (0, n2) and tail is None
+            Aht = None
+            if tail is not None:
+                Aht = torch.empty(A_tail.shape, dtype=torch.float32, pin_memory=True)
+                Aht.copy_(A_tail)
 
             def e2e_step():
                 if W["nystrom"] and host_row_layout:
@@ -788,8 +806,10 @@ def main():
                         Ch.copy_(Cd, non_blocking=True)
                 elif host_row_layout:
                     local.apply_host(Ah, out=Bh, sync=False)
-                else:  # column / 2D layouts: stage this rank's block, then the device path
+                else:  # column / 2D / balanced layouts: stage this rank's block(s), then the device path
                     A.copy_(Ah, non_blocking=True)
+                    if Aht is not None:
+                        A_tail.copy_(Aht, non_blocking=True)
                     o = step()
                     Bh[: o[0].shape[0]].copy_(o[0], non_blocking=True)
                     if o[2] is not None:
@@ -811,7 +831,7 @@ def main():
                 tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
             te = float(te.item())
             result["e2e"] = {"value": a_bytes_total / (te * 1e-3) / 1e9, "unit": "GB/s",
-                             "h2d_bytes_per_step": int(A.numel() * 4),
+                             "h2d_bytes_per_step": int(A.numel() * 4 + (A_tail.numel() * 4 if A_tail is not None else 0)),
                              "d2h_bytes_per_step": int(Bh.numel() * 4 + (Ch.numel() * 4 if W["nystrom"] else 0)),
                              "ms_per_step": te,
                              "path": ("nystrom_core_host / sketch_apply_host (C ABI, pinned host A streamed in row "

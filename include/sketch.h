@@ -164,6 +164,14 @@ sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, 
  * SK_ERR_SHAPE_MISMATCH, SK_ERR_ALIGNMENT, SK_ERR_CUDA (e.g. no multicast support). */
 sk_status_t sketch_multimem_sum(const float* mc_src, int64_t elems, float* out, float* mc_out, void* stream);
 
+/* Launch plan of sketch_apply_block for an m x k block (workspace unlimited): rows of A per work unit
+ * (rows that share each generated Omega slice: 128 x CTA group x accumulators x cluster pairs), the
+ * split / stream-K pieces per m-block, the CTA pairs per cluster, and the grid.  Any output pointer
+ * may be NULL.  Used by the distributed layer to cut row blocks at whole units.  Host only, no launch.
+ * Errors: SK_ERR_INVALID_VALUE. */
+sk_status_t sketch_plan_info(sk_sketch_t h, int64_t m, int64_t k, int32_t* rows_per_unit, int32_t* split,
+                             int32_t* cluster_pairs, int32_t* grid);
+
 /* Pack of the Redist variant's All-to-All ("unpack" step PAPER.md:1536): for column
  * bounds cb[0] = 0 < cb[1] < ... < cb[nblk] <= ldb, writes block j = B[0:rows, cb[j]:cb[j+1]]
  * row-major and contiguous at out + rows * cb[j] (out holds rows * cb[nblk] floats), so that each

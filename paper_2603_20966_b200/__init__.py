@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = (
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation", "sketch_set_trace",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
     "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
-    "sketch_rs_split", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers", "sketch_multimem_sum", "sketch_pack_cols",
+    "sketch_rs_split", "sketch_plan_info", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers", "sketch_multimem_sum", "sketch_pack_cols",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
     "sketch_status_string", "sketch_last_error", "sketch_build_info",
@@ -88,6 +88,8 @@ def load_library(build_if_missing: bool = True):
         lib.sketch_reduce_slots.argtypes = [vp, vp, i32, i64, i64, vp, i64, vp]
         lib.sketch_sum_peers.argtypes = [ctypes.POINTER(vp), i32, i64, vp, vp]
         lib.sketch_multimem_sum.argtypes = [vp, i64, vp, vp, vp]
+        lib.sketch_plan_info.argtypes = [vp, i64, i64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         lib.sketch_pack_cols.argtypes = [vp, i64, i64, ctypes.POINTER(i64), i32, vp, vp]
         lib.sketch_set_trace.argtypes = [vp, vp, i32]
         lib.sketch_generate.argtypes = [vp, i64, i64, i64, i64, vp, i64, vp]
@@ -257,6 +259,13 @@ class Sketch:
         v = ctypes.c_int32(0)
         _check(self._lib.sketch_rs_split(self._h, ctypes.c_int64(m), ctypes.c_int64(k), ctypes.byref(v)))
         return int(v.value)
+
+    def plan_info(self, m: int, k: int) -> dict:
+        """The library's launch plan for an m x k block (sketch_plan_info): rows_per_unit, split,
+        cluster_pairs, grid.  Host-side query, no GPU work."""
+        v = [ctypes.c_int32(0) for _ in range(4)]
+        _check(self._lib.sketch_plan_info(self._h, ctypes.c_int64(m), ctypes.c_int64(k), *[ctypes.byref(x) for x in v]))
+        return dict(zip(("rows_per_unit", "split", "cluster_pairs", "grid"), (int(x.value) for x in v)))
 
     def apply_block_rs(self, A_blk, k0: int, dst_ptrs, piece_rows: int, slot: int, slot_elems: int, split: int,
                        stream=None):

@@ -790,6 +790,18 @@ sk_status_t sketch_apply_block(sk_sketch_t h, const float* A_blk, int64_t m, int
                       static_cast<cudaStream_t>(stream));
 }
 
+sk_status_t sketch_plan_info(sk_sketch_t h, int64_t m, int64_t k, int32_t* rows_per_unit, int32_t* split,
+                             int32_t* cluster_pairs, int32_t* grid) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (m < 1 || k < 1) return fail(SK_ERR_INVALID_VALUE, "bad plan query");
+    const SketchPlan P = plan_sketch(h, m, k, 0, ~size_t(0));
+    if (rows_per_unit) *rows_per_unit = P.rows_per_unit;
+    if (split) *split = P.split;
+    if (cluster_pairs) *cluster_pairs = P.cl;
+    if (grid) *grid = P.grid;
+    return SK_SUCCESS;
+}
+
 sk_status_t sketch_rs_split(sk_sketch_t h, int64_t m, int64_t k, int32_t* split) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
     if (!split || m < 1 || k < 1) return fail(SK_ERR_INVALID_VALUE, "bad reduce-scatter split query");

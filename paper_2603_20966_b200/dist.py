@@ -81,7 +81,8 @@ class Layout:
         return Layout(a, b)
 
 
-def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool, variant: str = "noredist") -> int:
+def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool, variant: str = "noredist",
+                             tail_rows: int = 0) -> int:
     """Alg. 1 reduce-scatter volume (1 - 1/p2) n1 r / p1 words (+ r^2 AllReduce payload), fp32.
     Redist (row-block only): All-to-All of B, (1 - 1/P) n r / P words sent per rank,
     plus the all-gather that replicates C, (P - 1) r ceil(r / P) words."""
@@ -90,6 +91,7 @@ def predicted_bytes_per_rank(n1: int, r: int, layout: Layout, nystrom: bool, var
         return int(4 * ((n1 * r) // P - (n1 // P) * (r // P) + (P - 1) * r * (-(-r // P)))) if (n1 % P == 0 and r % P == 0) \
             else -1
     words = (1.0 - 1.0 / layout.p2) * n1 * r / layout.p1
+    words += tail_rows * r  # balanced row-block: this rank's partial of the tail rows
     if nystrom and P > 1:
         words += r * r
     return int(round(4 * words))
@@ -293,7 +295,7 @@ class DistSketch:
 
     def __init__(self, seed: int, dist, n1: int, n2: int, r: int, layout: Layout, group=None,
                  mode: str = "tf32", omega: str = "accurate", local=None, col_align: int = 128,
-                 fused_rs=False, fused_ar: bool = False, comm=None):
+                 fused_rs=False, fused_ar: bool = False, comm=None, balance_unit: int = 0):
         self.comm = comm if comm is not None else TorchComm(group)
         self.rank = self.comm.rank
         self.world = self.comm.world
@@ -304,6 +306,23 @@ class DistSketch:
         self.i, self.j = layout.coords(self.rank)
         self.row_bnd = balanced_split(n1, layout.p1)
         self.col_bnd = balanced_split(n2, layout.p2, col_align)
+        # Row-block layout cut at whole cluster units (balance_unit = rows that share each generated
+        # Omega slice in the library's plan, Sketch.plan_info): rank q owns rows [q M, (q+1) M), M a
+        # multiple of the unit, and the ragged tail of R = n1 - P M rows is split by COLUMNS -- every
+        # rank sketches the tail rows over its 1/P of K (Alg. 1 on a P x 1 grid for the bulk and a
+        # 1 x P grid for the tail) and the partials are reduced onto the last rank,
+        # whose B rows [(P-1) M, n1) stay contiguous.  Every rank then runs exactly M / unit units of
+        # full-K work plus a small tail launch, instead of ceil((n1 / P) / unit) units.
+        self.tail = None
+        self._tail_slots = None
+        self._tail_k = 0
+        if balance_unit and layout.p2 == 1 and self.world > 1:
+            U, P = int(balance_unit), self.world
+            M = (n1 // (P * U)) * U
+            R = n1 - P * M
+            if M > 0 and R > 0:
+                self.row_bnd = [q * M for q in range(P)] + [n1]
+                self.tail = {"M": M, "R": R, "cols": balanced_split(n2, P, col_align)}
         if local is None:
             from . import Sketch
             local = Sketch(seed, dist, n2, r, mode=mode, omega=omega)
@@ -365,9 +384,20 @@ class DistSketch:
 
     # ------------------------------------------------------------------ partition
     def a_block_range(self) -> tuple:
-        """(row0, row1, col0, col1) of A_ij owned by this rank."""
+        """(row0, row1, col0, col1) of A_ij owned by this rank (the bulk block for a balanced layout)."""
+        if self.tail is not None:
+            M = self.tail["M"]
+            return self.i * M, (self.i + 1) * M, 0, self.n2
         return (self.row_bnd[self.i], self.row_bnd[self.i + 1],
                 self.col_bnd[self.j], self.col_bnd[self.j + 1])
+
+    def tail_block_range(self):
+        """(row0, row1, col0, col1) of this rank's block of the ragged tail rows (balanced row-block
+        layout), or None."""
+        if self.tail is None:
+            return None
+        P, M, cols = self.world, self.tail["M"], self.tail["cols"]
+        return P * M, self.n1, cols[self.rank], cols[self.rank + 1]
 
     def b_piece_rows(self) -> tuple:
         """Global rows of B this rank owns after the reduce-scatter: piece j of R_i."""
@@ -379,9 +409,12 @@ class DistSketch:
         return a, min(r1, a + per)
 
     # ------------------------------------------------------------------ Alg. 1
-    def apply(self, A_blk):
-        """Returns (B_piece, (row0, row1)): the rows of B = A Omega this rank owns."""
+    def apply(self, A_blk, A_tail=None):
+        """Returns (B_piece, (row0, row1)): the rows of B = A Omega this rank owns.  A balanced row-block
+        layout also takes this rank's block of the tail rows (tail_block_range)."""
         import torch
+        if self.tail is not None:
+            return self._apply_balanced(A_blk, A_tail)
         r0, r1, c0, c1 = self.a_block_range()
         assert tuple(A_blk.shape) == (r1 - r0, c1 - c0), (A_blk.shape, (r1 - r0, c1 - c0))
         p2 = self.layout.p2
@@ -441,6 +474,45 @@ class DistSketch:
         self.comm_bytes += 4 * per * r * (p2 - 1)
         return piece[: b - a], (a, b)
 
+    def _apply_balanced(self, A_blk, A_tail):
+        """Balanced row-block (see __init__): the tail partial first (so every rank reaches the barrier
+        together), then the bulk rows; the last rank sums the P tail partials into the end of its B."""
+        import torch
+        T, r, P = self.tail, self.r, self.world
+        M, R = T["M"], T["R"]
+        t0, t1, c0, c1 = self.tail_block_range()
+        assert A_tail is not None and tuple(A_tail.shape) == (t1 - t0, c1 - c0), "tail block expected"
+        assert tuple(A_blk.shape) == (M, self.n2), (A_blk.shape, (M, self.n2))
+        owner = self.rank == P - 1
+        dev = A_blk.device
+        sb = None
+        if r % 4 == 0 and getattr(A_blk, "is_cuda", False):
+            if self._tail_slots is None:
+                self._tail_slots = self._symm(self.comm, (2, R * r), dev, "tail reduction") or False
+            sb = self._tail_slots or None
+        if sb is not None:
+            k = self._tail_k
+            self._tail_k ^= 1
+            part = sb.tensor[k].view(R, r)
+            self.local.apply_block(A_tail, c0, out=part)
+            sb.barrier()  # every rank's tail partial is in its slot k
+        else:
+            part = self.local.apply_block(A_tail, c0)
+        Bp = torch.empty((M + R, r), dtype=torch.float32, device=dev) if owner else None
+        if owner:
+            self.local.apply_block(A_blk, 0, out=Bp[:M])
+        else:
+            Bp = self.local.apply_block(A_blk, 0)
+        if sb is not None:
+            if owner:
+                self._reduce(sb, k * R * r * 4, R * r, Bp[M:])
+        else:
+            self.comm.all_reduce(part)
+            if owner:
+                Bp[M:].copy_(part)
+        self.comm_bytes += 4 * R * r  # this rank's tail partial handed to the reduction
+        return Bp, self.b_piece_rows()
+
     def _reduce(self, sb, off: int, elems: int, out):
         """out[:elems] = sum over the group of the symmetric buffers at byte offset `off`: inside the
         NVSwitch through the multicast mapping (NVLS, `sketch_multimem_sum`) when the group has one,
@@ -488,12 +560,12 @@ class DistSketch:
         return piece, (a, b)
 
     # ------------------------------------------------------------------ Alg. 2 (Redist)
-    def nystrom_core_redist(self, A_blk):
+    def nystrom_core_redist(self, A_blk, A_tail=None):
         """Redist variant: returns (B_piece, rows, C) like nystrom_core (row-block layout only)."""
         import torch
         if self.layout.p2 != 1:
             raise ValueError("the Redist variant runs on the row-block grid Pi = (P, 1, 1)")
-        Bp, (a, b) = self.apply(A_blk)
+        Bp, (a, b) = self.apply(A_blk, A_tail)
         P, r = self.world, self.r
         if P == 1:
             return Bp, (a, b), self.local.core_block(Bp, a)
@@ -522,7 +594,7 @@ class DistSketch:
         return Bp, (a, b), C
 
     # ------------------------------------------------------------------ Alg. 2 (No-Redist)
-    def nystrom_core(self, A_blk):
+    def nystrom_core(self, A_blk, A_tail=None):
         """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank.
 
         2D / column layouts with the peer-read reduce-scatter and the fused AllReduce overlap the two
@@ -538,7 +610,7 @@ class DistSketch:
         self._overlap_rs = overlap
         self._last_bbar = None
         try:
-            Bp, (a, b) = self.apply(A_blk)
+            Bp, (a, b) = self.apply(A_blk, A_tail)
         finally:
             self._overlap_rs = False
         if overlap and self._last_bbar is not None:

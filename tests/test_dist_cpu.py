@@ -180,3 +180,37 @@ def test_virtual_comm_matches_oracle(world, spec, variant):
         assert comm == predicted_bytes_per_rank(n, r, layout, True, variant)
         covered[a:b] += 1
     assert np.all(covered == 1)
+
+
+@pytest.mark.parametrize("world,unit,variant", [(2, 128, "noredist"), (4, 128, "noredist"), (4, 64, "redist"),
+                                                (8, 32, "noredist")])
+def test_balanced_rowblock_matches_oracle(world, unit, variant):
+    """Row-block cut at whole units with the ragged tail split by columns and reduced onto the last rank
+    (virtual ranks, oracle stand-in): B pieces partition the rows, B and C exact in the integer regime,
+    bytes = the tail partial (+ r^2 for C, or the Redist exchange)."""
+    from paper_2603_20966_b200.dist import run_virtual
+    n, r = 1120, 24
+    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+    Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
+    layout = Layout.parse("row", world)
+
+    def body(comm):
+        ds = DistSketch(SEED, "rademacher", n, n, r, layout, local=OracleLocal(SEED, "rademacher", r), comm=comm,
+                        balance_unit=unit)
+        assert ds.tail is not None
+        r0, r1, c0, c1 = ds.a_block_range()
+        t0, t1, tc0, tc1 = ds.tail_block_range()
+        Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1]))
+        At = torch.from_numpy(np.ascontiguousarray(A[t0:t1, tc0:tc1]))
+        f = ds.nystrom_core_redist if variant == "redist" else ds.nystrom_core
+        Bp, (a, b), C = f(Ablk, At)
+        return a, b, Bp.numpy(), C.numpy(), ds.comm_bytes, ds.tail["R"]
+
+    covered = np.zeros(n, dtype=int)
+    for a, b, Bp, C, comm, R in run_virtual(world, body):
+        assert np.array_equal(Bp.astype(np.float64), Bref[a:b])
+        assert np.array_equal(C.astype(np.float64), Cref)
+        if variant == "noredist":
+            assert comm == predicted_bytes_per_rank(n, r, layout, True, tail_rows=R)
+        covered[a:b] += 1
+    assert np.all(covered == 1)

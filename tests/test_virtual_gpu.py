@@ -155,3 +155,35 @@ def test_virtual_epilogue_rs_tf32x3(world, spec):
     Bref = oracle.sketch(SEED, "rademacher", A, r)
     res = _run(world, spec, n1, n2, r, "rademacher", "tf32x3", A, rs="epilogue")
     _check_exact(res, Bref, None, n1)
+
+
+@pytest.mark.parametrize("world,mode", [(2, "tf32"), (4, "bf16"), (8, "tf32")])
+def test_virtual_balanced_rowblock_exact(world, mode):
+    """Row-block cut at whole units of the library's own plan (Sketch.plan_info), the ragged tail split
+    by columns and reduced onto the last rank through symmetric memory (real kernels): exact B and C."""
+    import paper_2603_20966_b200 as sk
+    from paper_2603_20966_b200.dist import DistSketch, Layout, run_virtual
+    n, r = 3300, 48
+    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+    Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
+    torch.cuda.set_device(0)
+
+    def body(comm):
+        local = sk.Sketch(SEED, "rademacher", n, r, mode=mode)
+        unit = local.plan_info(-(-n // world), n)["rows_per_unit"]
+        ds = DistSketch(SEED, "rademacher", n, n, r, Layout.parse("row", world), local=local, fused_ar=True,
+                        comm=comm, balance_unit=unit)
+        r0, r1, c0, c1 = ds.a_block_range()
+        t = ds.tail_block_range()
+        Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1])).cuda()
+        At = torch.from_numpy(np.ascontiguousarray(A[t[0]:t[1], t[2]:t[3]])).cuda() if t else None
+        outs = []
+        for _ in range(3):
+            Bp, (a, b), C = ds.nystrom_core(Ablk, At)
+            torch.cuda.current_stream().synchronize()
+            outs.append((a, b, Bp.cpu().numpy(), C.cpu().numpy()))
+        return {"outs": outs, "tail": ds.tail is not None, "fallbacks": list(ds.fallbacks)}
+
+    res = run_virtual(world, body)
+    assert all(rk["tail"] for rk in res) and not any(rk["fallbacks"] for rk in res)
+    _check_exact(res, Bref, Cref, n)
