@@ -163,7 +163,7 @@ def test_virtual_balanced_rowblock_exact(world, mode):
     by columns and reduced onto the last rank through symmetric memory (real kernels): exact B and C."""
     import paper_2603_20966_b200 as sk
     from paper_2603_20966_b200.dist import DistSketch, Layout, run_virtual
-    n, r = 3300, 48
+    n, r = 4400, 48  # units of 512 rows (pairs, 2 accumulators): 2048 / 1024 / 512 rows per rank + 304 tail
     A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
     Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
     torch.cuda.set_device(0)
