@@ -411,9 +411,10 @@ def main():
     ap.add_argument("--omega-ablation", action="store_true",
                     help="f4: also time B = A*Omega with Omega materialised in HBM (+ all-gathered over NCCL "
                          "when N > 1) and a cuBLAS GEMM, against the fused in-kernel regeneration")
-    ap.add_argument("--no-balance", action="store_true",
-                    help="row-block grids: plain balanced row split instead of whole cluster units per rank with "
-                         "the ragged tail rows split by columns")
+    ap.add_argument("--balance", action="store_true",
+                    help="row-block grids: whole cluster units per rank with the ragged tail rows split by columns "
+                         "and reduced onto the last rank (measured no faster at 2 / 4 GPUs: the tail launch's "
+                         "unshared Omega costs what the saved unit saves), instead of the plain balanced row split")
     ap.add_argument("--no-other-modes", action="store_true",
                     help="skip timing the other precision modes / transforms after the main line")
     args = ap.parse_args()
@@ -456,7 +457,7 @@ def main():
     local = sk.Sketch(SEED_OMEGA, W["dist"], n2, r, mode=args.mode, omega=args.omega, split_k=args.split_k)
     # row-block grids cut at whole units of the library's plan (the ragged tail split by columns)
     unit = 0
-    if layout.p2 == 1 and world > 1 and not args.no_balance:
+    if layout.p2 == 1 and world > 1 and args.balance:
         unit = local.plan_info(-(-n1 // world), n2)["rows_per_unit"]
     ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.rs,
                     fused_ar=not args.nccl_ar, balance_unit=unit)
