@@ -53,15 +53,21 @@ NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25  # B200 dense tensor peaks (B200_PROFILING.m
 
 
 def auto_layout(wl_name, world):
-    """The processor grid for BASELINE.json's configs.  c2 ("2/4/8 with 2D grid") and c5: the p1 x p2
-    grid the paper's own selection rule picks (sec. 4.3: Case 1, p = (P, 1, 1), whenever
-    P <= n1 -- the communication lower bound for B is then zero, Thm 4.2); the square
-    grids (2x2, 4x2) stay available via --layout.  c3 row-block (zero communication), c4 column-block
-    (reduce-scatter of B), as BASELINE.json names them."""
+    """The processor grid BASELINE.json's configs name: c2 ("2/4/8 with 2D grid") and c5 ("2D grid"): the
+    most square p1 x p2 grid with p1 >= p2 (2x1, 2x2, 4x2); c3 row-block (zero communication); c4
+    column-block (reduce-scatter of B).  The grid the paper's own selection rule picks for P <= n1
+    (sec. 4.3 Case 1: P x 1, zero words for B) is `--layout row` (measured faster
+    at 4 GPUs: 0.552 vs 0.564 ms)."""
     if world == 1:
         return "row"
     if wl_name == "c4":
         return "col"
+    if wl_name in ("c2", "c5"):
+        p2 = 1
+        for d in range(1, int(world ** 0.5) + 1):
+            if world % d == 0:
+                p2 = d
+        return f"{world // p2}x{p2}"
     return "row"
 
 
@@ -391,8 +397,8 @@ def main():
                          "mode, whose RN rounding of Omega to bf16 (2^-9) hides it (same relF of B as accurate), "
                          "accurate (<= 2 ulp fp32) in tf32 / tf32x3 (reading R5)")
     ap.add_argument("--layout", default="auto",
-                    help="row | col | AxB (p1 x p2) | auto = c2 / c5: the grid of the paper's sec. 4.3 rule "
-                         "(P x 1 for P <= n1), c3: row-block, c4: column-block")
+                    help="row | col | AxB (p1 x p2) | auto = the grid BASELINE.json names: c2 / c5 the most "
+                         "square 2D grid, c3 row-block, c4 column-block")
     ap.add_argument("--split-k", type=int, default=0)
     ap.add_argument("--variant", default="noredist", choices=["noredist", "redist"],
                     help="Alg. 2 variant for N > 1 row-block Nystrom (PAPER.md:698)")
@@ -653,7 +659,7 @@ def main():
                    "omega_transform": args.omega, "layout": f"{layout.p1}x{layout.p2}",
                    "row_split": (f"{ds.tail['M']} rows per rank (whole units of {unit}) + the {ds.tail['R']}-row tail "
                                  f"split by columns, reduced onto rank {world - 1}" if ds.tail else "balanced"),
-                   "layout_rule": ("paper sec. 4.3 grid selection: Case 1 (P x 1) since P <= n1 (PAPER.md:438-440)"
+                   "layout_rule": ("BASELINE.json's 2D grid (most square p1 x p2, p1 >= p2)"
                                    if args.layout == "auto" and W["nystrom"] else args.layout),
                    "l2": "inputs larger than L2 (A = %.1f GB)" % (a_bytes_total / 1e9) if a_bytes_total > 126e6
                    else "A fits in L2 (c1: launch-latency bound)"},
