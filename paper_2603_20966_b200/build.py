@@ -44,6 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
         if os.environ.get("SK_BUILD_TRACE"):  # diagnostics build: per-stage pipeline trace compiled in
             cmd.append("-DSK_TRACE")
+        if os.environ.get("SK_EXTRA_NVCC_FLAGS"):  # tuning builds (e.g. -DSK_RNG_WARPS_BF16=20), never the product
+            cmd += os.environ["SK_EXTRA_NVCC_FLAGS"].split()
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

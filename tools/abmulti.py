@@ -26,9 +26,10 @@ class Sampler:
         self.t = threading.Thread(target=f, daemon=True); self.t.start(); return self
     def __exit__(self, *a):
         self.run = False; self.t.join()
-n, r = int(os.environ.get("N", 50000)), 256
-A = torch.empty((n, n), device='cuda').uniform_(-0.5, 0.5)
-B = torch.empty((n, r), device='cuda')
+n, r = int(os.environ.get("N", 50000)), int(os.environ.get("R", 256))
+n1 = int(os.environ.get("N1", n))  # A is n1 x n (N1 / N / R env: any shape)
+A = torch.empty((n1, n), device='cuda').uniform_(-0.5, 0.5)
+B = torch.empty((n1, r), device='cuda')
 cfgs = json.loads(os.environ.get("CFGS", '[["tf32","fast",0],["tf32","fast",7],["bf16","accurate",0]]'))
 res = {}
 for rnd in range(int(os.environ.get("ROUNDS", 3))):
