@@ -39,6 +39,9 @@ constexpr int kRngWarps = 16;  // Omega producers (the first 4 also run the epil
 // 8 warps 1.930 vs 16 warps 1.974 ms; the two-column-block c4 shape 12 warps 2.784 vs 2.844 ms.
 // SK_RNG_WARPS_BF16 (compile-time) overrides both for tuning builds.
 constexpr int rng_warps(int mode, int ncol = 1) {
+#ifdef SK_RNG_WARPS_TF32
+    if (mode == kTF32) return SK_RNG_WARPS_TF32;  // tuning builds only
+#endif
 #ifdef SK_RNG_WARPS_BF16
     return mode == kBF16 ? SK_RNG_WARPS_BF16 : kRngWarps;
 #else
