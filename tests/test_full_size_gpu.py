@@ -61,3 +61,39 @@ def test_c3_full_size_integer_exact():
     assert torch.equal(B, B.round()) and float(B.abs().max()) <= 4 * n2
     del A, B
     torch.cuda.empty_cache()
+
+
+def test_c2_full_size_tf32x3():
+    """The API's default, fp32-accurate mode at c2's full size (K = 50,000 per B row: 49 promoted TMEM
+    chunks): sampled rows of B and all of C within the north star's 1e-5."""
+    import paper_2603_20966_b200 as sk
+    n, r = 50000, 256
+    A = torch.empty((n, n), dtype=torch.float32, device="cuda")
+    synth.rbf_kernel_device(2, n, 3072, out=A)
+    s = sk.Sketch(SEED, "gaussian", n, r, mode="tf32x3")
+    B, C = s.nystrom_core(A)
+    torch.cuda.synchronize()
+    rows = sorted(set(np.linspace(0, n - 1, 16).astype(int).tolist()) | {1, n - 2})
+    Bref = oracle.sketch(SEED, "gaussian", A[rows].cpu().numpy(), r)
+    assert _relF(B[rows].cpu().numpy(), Bref) <= 1e-5
+    Cown = oracle.core(SEED, "gaussian", B.double().cpu().numpy(), 0)
+    assert _relF(C.double().cpu().numpy(), Cown) <= 1e-5
+    del A
+    torch.cuda.empty_cache()
+
+
+def test_c4_full_size_sampled_rows():
+    """c4 at full size (2,048 x 4,000,000, r = 512 Gaussian, bf16 / fast): ONE pass over A with two N = 256
+    column blocks per CTA, in the bench's launch configuration; sampled rows against the oracle (which
+    materialises Omega for all 4M rows in fp64 -- 16 GB of host memory -- so only a few rows)."""
+    import paper_2603_20966_b200 as sk
+    n1, n2, r = 2048, 4_000_000, 512
+    A = synth.uniform_device(4, n1, n2)
+    s = sk.Sketch(SEED, "gaussian", n2, r, mode="bf16", omega="fast")
+    B = s.apply(A)
+    torch.cuda.synchronize()
+    rows = [0, 777, 2047]
+    Bref = oracle.sketch(SEED, "gaussian", A[rows].cpu().numpy(), r)
+    assert _relF(B[rows].cpu().numpy(), Bref) <= TOL
+    del A
+    torch.cuda.empty_cache()
