@@ -38,10 +38,13 @@ constexpr int kRngWarps = 16;  // Omega producers (the first 4 also run the epil
 // differs with the tile (same-box A/B of 8 / 10 / 12 / 14 / 16, r2af-r2ah): c2 (one column block)
 // 8 warps 1.930 vs 16 warps 1.974 ms; the two-column-block c4 shape 12 warps 2.784 vs 2.844 ms.
 // SK_RNG_WARPS_BF16 (compile-time) overrides both for tuning builds.
-constexpr int rng_warps(int mode, int ncol = 1) {
+// tf32 with the fast transform: 8 warps (2.493 -> 2.437 ms at c2); with the accurate one 16 stay best
+// (2.520 vs 2.691 ms with 8; r2ai).
+constexpr int rng_warps(int mode, int ncol = 1, bool fast = false) {
 #ifdef SK_RNG_WARPS_TF32
     if (mode == kTF32) return SK_RNG_WARPS_TF32;  // tuning builds only
 #endif
+    if (mode == kTF32 && fast && ncol == 1) return 8;
 #ifdef SK_RNG_WARPS_BF16
     return mode == kBF16 ? SK_RNG_WARPS_BF16 : kRngWarps;
 #else
@@ -50,7 +53,9 @@ constexpr int rng_warps(int mode, int ncol = 1) {
 }
 // bf16 / tf32x3: warps converting each fp32 A stage (bf16 operand / A_lo)
 constexpr int cvt_warps(int mode) { return (mode == kBF16 || mode == kTF32x3) ? SK_CVT_WARPS_BF16 : 0; }
-constexpr int threads_for(int mode, int ncol = 1) { return (kCtlWarps + rng_warps(mode, ncol) + cvt_warps(mode)) * 32; }
+constexpr int threads_for(int mode, int ncol = 1, bool fast = false) {
+    return (kCtlWarps + rng_warps(mode, ncol, fast) + cvt_warps(mode)) * 32;
+}
 
 // diagnostics (sketch_set_trace, compiled in only with -DSK_TRACE: even a predicated-off check
 // slows the single-thread TMA / MMA loops measurably): %globaltimer stamp of event `ev`, stage `i`
@@ -165,7 +170,7 @@ __host__ __device__ inline SmemLayout make_layout(int nacc, int npad, int a_stag
 // pass over A for r <= 512 (c4); with CL = 8 (16-CTA clusters) every generated Omega element still
 // feeds 2048 rows of A.
 template <int CG, int NACC, int DIST, int MODE, bool FAST, int CL = 1, int NCOL = 1>
-__global__ void __launch_bounds__(threads_for(MODE, NCOL), 1)
+__global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
     sketch_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const SketchGemmParams p) {
     static_assert(CL == 1 || CG == 2, "Omega sharing between pairs needs CTA pairs");
     static_assert(CL >= 1 && CL <= 8, "1 to 8 CTA pairs per cluster");
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL), 1)
     constexpr int NBOX = KS / 32;                          // 128-B TMA boxes per accumulator
     constexpr int NSUBO = T64 ? 2 : 1;                     // 32-K Omega sub-tiles per stage
     constexpr int KMMA = T64 ? 8 : 4;                      // MMAs (per accumulator) per stage
-    constexpr int kRngW = rng_warps(MODE, NCOL);           // Omega producer warps
+    constexpr int kRngW = rng_warps(MODE, NCOL, FAST);     // Omega producer warps
     constexpr int kRngThreads = kRngW * 32;
     constexpr int kCvtWarps = cvt_warps(MODE);             // bf16 converter warps
     const int nh = p.npad / CG;        // Omega columns of one N block held by this CTA
@@ -879,7 +884,7 @@ int sketch_gemm_max_clusters(int cg, int nacc, int dist, int mode, bool fast, in
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cg * cl * 16);
-    cfg.blockDim = dim3(threads_for(mode, ncol));
+    cfg.blockDim = dim3(threads_for(mode, ncol, fast && dist == kGaussian));
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -904,7 +909,7 @@ cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p
     if (cudaError_t e = prepare_kernel(fn, smem, cg * cl)) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads_for(mode, ncol));
+    cfg.blockDim = dim3(threads_for(mode, ncol, fast && dist == kGaussian));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
