@@ -368,11 +368,9 @@ CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0, int64_t nb =
     CorePlan C{};
     C.tc = true;
     C.npad = static_cast<int>(std::min<int64_t>(x3 ? 128 : 256, round_up(nb, 16)));
+    C.nacc = (!x3 && h->r > 128) ? 2 : 1;
     C.base = i0 & ~static_cast<int64_t>(127);
     const int64_t span = std::max<int64_t>(1, i0 + m - C.base);
-    // two 128-column halves of Omega per CTA, unless B is short: then one half per CTA (grid.y = 2),
-    // so each CTA regenerates half the Omega tile and twice as many CTAs share the rows
-    C.nacc = (!x3 && h->r > 128 && span >= 256LL * sk::num_sms()) ? 2 : 1;
     const int64_t blocks = ((h->r + 128 * C.nacc - 1) / (128 * C.nacc)) * ((nb + C.npad - 1) / C.npad);
     const int64_t want = std::max<int64_t>(1, sk::num_sms() / blocks);
     C.step = round_up((span + want - 1) / want, 128);

@@ -223,46 +223,13 @@ cudaError_t launch_pack_cols(const float* B, int64_t rows, int64_t ldb, const in
 }
 
 // C[a, b] = sum_{c < chunks} part[c][a][b], r x nb, fixed order.
-// Loads are issued 8 chunks ahead of the (in-order) adds, 4 elements per thread when nb % 4 == 0:
-// the per-element sum order stays chunk 0, 1, 2, ... (fixed), but the chunk loads overlap.
 __global__ void core_reduce_kernel(const float* __restrict__ part, int32_t chunks, int32_t r, int32_t nb,
                                    float* __restrict__ C, int64_t ldc) {
     const int64_t rr = static_cast<int64_t>(r) * nb;
-    constexpr int kU = 8;
-    if ((nb & 3) == 0 && (ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
-        (reinterpret_cast<uintptr_t>(part) & 15) == 0) {
-        const int64_t rr4 = rr / 4;
-        const float4* p4 = reinterpret_cast<const float4*>(part);
-        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rr4;
-             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int c0 = 0; c0 < chunks; c0 += kU) {
-                float4 v[kU];
-#pragma unroll
-                for (int u = 0; u < kU; ++u)
-                    v[u] = (c0 + u < chunks) ? __ldg(p4 + (c0 + u) * rr4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int u = 0; u < kU; ++u)
-                    if (c0 + u < chunks) {
-                        acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
-                    }
-            }
-            const int64_t idx = 4 * i;
-            *reinterpret_cast<float4*>(C + (idx / nb) * ldc + idx % nb) = acc;
-        }
-        return;
-    }
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < rr;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float acc = 0.f;
-        for (int c0 = 0; c0 < chunks; c0 += kU) {
-            float v[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) v[u] = (c0 + u < chunks) ? __ldg(part + (c0 + u) * rr + idx) : 0.f;
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-                if (c0 + u < chunks) acc += v[u];
-        }
+        for (int c = 0; c < chunks; ++c) acc += __ldg(part + c * rr + idx);
         C[(idx / nb) * ldc + idx % nb] = acc;
     }
 }
