@@ -659,18 +659,24 @@ class DistSketch:
 
 
 def run_virtual(world: int, fn, timeout: float = 600.0):
-    """Runs fn(comm) for `world` virtual ranks (threads, each on its own CUDA stream of the current
-    device when CUDA is available); returns the results in rank order, re-raising the first error."""
+    """Runs fn(comm) for `world` virtual ranks (threads of this process on the current device when CUDA
+    is available); returns the results in rank order, re-raising the first error.
+
+    All virtual ranks enqueue on ONE shared CUDA stream: the persistent sketch kernel's CTAs may wait on
+    one another inside a launch (in-place pieces, sketch_gemm.cu), which is safe only while the grid is
+    co-resident -- two such launches running concurrently on one GPU could each hold the SMs the other
+    waits for.  Serialising the ranks' kernels on one stream keeps every launch alone on the device."""
     import torch
     vw = VirtualWorld(world)
     res, errs = [None] * world, [None] * world
     dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+    shared = torch.cuda.Stream(device=dev) if dev is not None else None
 
     def body(rank):
         try:
             if dev is not None:
                 torch.cuda.set_device(dev)
-                s = torch.cuda.Stream()
+                s = shared
                 with torch.cuda.stream(s):
                     res[rank] = fn(VirtualComm(vw, rank))
                     s.synchronize()
