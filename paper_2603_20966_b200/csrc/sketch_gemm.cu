@@ -912,7 +912,7 @@ cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p
     cfg.blockDim = dim3(threads_for(mode, ncol, fast && dist == kGaussian));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     // ablation bit 3: launch single-CTA tiles as clusters of 2 (isolates cluster placement effects)
     attr[0].val.clusterDim.x = (cg == 1 && (p.ablate & 8u)) ? 2 : cg * cl;
@@ -920,6 +920,13 @@ cudaError_t launch_sketch_gemm(const CUtensorMap& tmA, const SketchGemmParams& p
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (p.inplace) {
+        // in-place pieces: CTAs wait for other CTAs of this grid, so the grid must be co-resident even
+        // when other kernels share the GPU -- a cooperative launch is scheduled only as a whole
+        attr[1].id = cudaLaunchAttributeCooperative;
+        attr[1].val.cooperative = 1;
+        cfg.numAttrs = 2;
+    }
     void* args[] = {const_cast<CUtensorMap*>(&tmA), const_cast<SketchGemmParams*>(&p)};
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
