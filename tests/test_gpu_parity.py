@@ -646,3 +646,37 @@ def test_ragged_row_remainder(mode, omega, n1):
     Ai = synth.int_matrix(24, n1, n2)
     Bi = sk.Sketch(SEED, "rademacher", n2, r, mode=mode).apply(_dev(Ai)).cpu().numpy()
     assert np.array_equal(Bi.astype(np.float64), oracle.sketch(SEED, "rademacher", Ai, r))
+
+
+@pytest.mark.timeout(300)
+def test_concurrent_inplace_launches_two_streams():
+    """Two in-place (stream-K / split-K, waiting pieces) sketch launches in flight at once on one GPU from
+    two streams and two threads: the launches are cooperative, so neither can hold SMs the other's
+    waiting CTAs need; both results equal the serial ones bit for bit."""
+    import threading
+    sk = _sk()
+    n1, n2, r = 12500, 25000, 256
+    A1 = synth.uniform_device(31, n1, n2)
+    A2 = synth.uniform_device(32, n1, n2)
+    s1 = sk.Sketch(SEED, "gaussian", n2, r, mode="bf16", omega="fast")
+    s2 = sk.Sketch(SEED + 1, "gaussian", n2, r, mode="bf16", omega="fast")
+    ref1, ref2 = s1.apply(A1), s2.apply(A2)
+    torch.cuda.synchronize()
+    outs = [None, None]
+
+    def run(i, s, A):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            B = None
+            for _ in range(20):
+                B = s.apply(A)
+            st.synchronize()
+        outs[i] = B
+
+    ts = [threading.Thread(target=run, args=(0, s1, A1)), threading.Thread(target=run, args=(1, s2, A2))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(240)
+    assert not any(t.is_alive() for t in ts)
+    assert torch.equal(outs[0], ref1) and torch.equal(outs[1], ref2)
