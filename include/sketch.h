@@ -29,9 +29,13 @@
  *     was enqueued.  Asynchronous device faults surface as SK_ERR_CUDA from a later call;
  *   - no exception crosses the ABI; sketch_last_error() gives a thread-local detail string;
  *   - handles are immutable after configuration (sketch_set_*) and may be used concurrently from
- *     several host threads on different streams.
- *   - results are deterministic: fixed-order split-K and core reductions, so identical calls give
- *     bit-identical outputs.
+ *     several host threads on different streams.  A sketch launch whose split / stream-K pieces
+ *     accumulate in place (2-4 pieces per m-block) has CTAs waiting on other CTAs of the same grid;
+ *     such launches are cooperative (the grid is scheduled only as a whole), so concurrent launches
+ *     on one device cannot deadlock;
+ *   - results are deterministic: fixed-order split-K / stream-K / in-place piece and core
+ *     reductions, so identical calls give bit-identical outputs (the one exception is the caller's
+ *     choice of sketch_multimem_sum, whose in-switch summation order is the hardware's).
  */
 #ifndef PAPER_2603_20966_B200_SKETCH_H
 #define PAPER_2603_20966_B200_SKETCH_H
