@@ -861,7 +861,18 @@ static const void* pick_kernel(int cg, int nacc, int dist, int mode, bool fast, 
 // ever raised) and, for clusters of more than 8 CTAs, the non-portable cluster size.
 static cudaError_t prepare_kernel(const void* fn, size_t smem, int cluster) {
     if (cudaError_t e = raise_smem_limit(fn, smem)) return e;
-    if (cluster > 8) return cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (cluster > 8) {
+        static std::mutex mu;
+        static std::map<std::pair<int, const void*>, bool> done;  // per (device, function), set once
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> g(mu);
+        bool& d = done[std::make_pair(dev, fn)];
+        if (!d) {
+            if (cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) return e;
+            d = true;
+        }
+    }
     return cudaSuccess;
 }
 
