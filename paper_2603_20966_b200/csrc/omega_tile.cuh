@@ -196,39 +196,6 @@ __device__ __forceinline__ void produce_omega_tile_bf16_g(uint8_t* tile, int64_t
     const uint32_t tile_base = smem_u32(tile);
     int n = n_start, j = j_start;
     constexpr int kJ = HALF ? 16 : 8;
-#ifdef SK_BF16_ILP2
-    if constexpr (!HALF) {
-        if (roff == 0) {
-            // two items per iteration: their four Philox / Box-Muller chains are independent
-#pragma unroll 1
-            while (j < kJ) {
-                int n2 = n + tr, j2 = j + tq;
-                if (n2 >= npad) { n2 -= npad; ++j2; }
-                const bool two = j2 < kJ;
-                const int n2c = two ? n2 : n, j2c = two ? j2 : j;
-                const uint32_t col1 = static_cast<uint32_t>(c0 + n), col2 = static_cast<uint32_t>(c0 + n2c);
-                const uint4 xa = philox_gauss_call(q0 + 2 * j, col1, key0, key1);
-                const uint4 xb = philox_gauss_call(q0 + 2 * j + 1, col1, key0, key1);
-                const uint4 xc = philox_gauss_call(q0 + 2 * j2c, col2, key0, key1);
-                const uint4 xd = philox_gauss_call(q0 + 2 * j2c + 1, col2, key0, key1);
-                const float4 a = values4<DIST, FAST>(xa), b = values4<DIST, FAST>(xb);
-                const float4 c = values4<DIST, FAST>(xc), d = values4<DIST, FAST>(xd);
-                const uint32_t row1 = tile_base + static_cast<uint32_t>(n) * 128u;
-                st_shared_v4_u32(row1 + ((static_cast<uint32_t>(j) ^ sw128_phase(row1)) << 4), pack_bf16x2(a.x, a.y),
-                                 pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
-                if (two) {
-                    const uint32_t row2 = tile_base + static_cast<uint32_t>(n2) * 128u;
-                    st_shared_v4_u32(row2 + ((static_cast<uint32_t>(j2) ^ sw128_phase(row2)) << 4), pack_bf16x2(c.x, c.y),
-                                     pack_bf16x2(c.z, c.w), pack_bf16x2(d.x, d.y), pack_bf16x2(d.z, d.w));
-                }
-                n = n2 + tr;
-                j = j2 + tq;
-                if (n >= npad) { n -= npad; ++j; }
-            }
-            return;
-        }
-    }
-#endif
 #pragma unroll 1
     while (j < kJ) {
         const uint32_t col = static_cast<uint32_t>(c0 + n);
