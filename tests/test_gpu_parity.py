@@ -680,3 +680,18 @@ def test_concurrent_inplace_launches_two_streams():
         t.join(240)
     assert not any(t.is_alive() for t in ts)
     assert torch.equal(outs[0], ref1) and torch.equal(outs[1], ref2)
+
+
+@pytest.mark.parametrize("mode", ["tf32", "bf16", "tf32x3"])
+def test_three_column_passes_with_pieces(mode):
+    """r = 600 (three 256-column passes, none a 512-column pair) on a shape the planner splits into
+    pieces: every pass accumulates its pieces (in place or through partials) into its own columns of B;
+    integer regime bit-exact, Gaussian within tolerance."""
+    sk = _sk()
+    n1, n2, r = 1500, 9000, 600
+    Ai = synth.int_matrix(41, n1, n2)
+    Bi = sk.Sketch(SEED, "rademacher", n2, r, mode=mode).apply(_dev(Ai)).cpu().numpy()
+    assert np.array_equal(Bi.astype(np.float64), oracle.sketch(SEED, "rademacher", Ai, r))
+    A = synth.uniform(42, n1, n2)
+    B = sk.Sketch(SEED, "gaussian", n2, r, mode=mode).apply(_dev(A)).cpu().numpy()
+    assert _relF(B, oracle.sketch(SEED, "gaussian", A, r)) <= TOL[mode]
