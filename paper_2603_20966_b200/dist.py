@@ -356,13 +356,7 @@ class DistSketch:
         # ... for groups of at least this many ranks (2 ranks: the NVLink peer read is as fast or faster,
         # r2j / r2p); SK_NVLS_MIN overrides
         self.nvls_min_ranks = int(os.environ.get("SK_NVLS_MIN", "4"))
-        # nystrom_core on 2D / column layouts: core GEMM on the local B-bar beside the B reduce-scatter
-        # (opt-in: at p2 = 2 the doubled core rows cost what the overlap saves -- 1x2 c2 at 2 GPUs:
-        # 1.099 ms with vs 1.085 ms without, r2o)
-        self.overlap_core = os.environ.get("SK_OVERLAP_CORE", "0") == "1"
-        self._side_stream = None
-        self._overlap_rs = False
-        self._last_bbar = None
+
         self.reduce_path = None  # "nvls" / "peer" once a symmetric-memory reduction ran
 
     # ------------------------------------------------------------------ symmetric memory setup
@@ -460,17 +454,10 @@ class DistSketch:
         sb = st["sb"]
         self.local.apply_block(A_blk, c0, out=sb.tensor[k][:rows])
         sb.barrier()  # every rank's B-bar is in its slot k
-        self._last_bbar = sb.tensor[k][:rows]  # this rank's own B-bar (nystrom_core's overlapped core)
         a, b = self.b_piece_rows()
         piece = torch.empty((per, r), dtype=torch.float32, device=A_blk.device)
         off = (k * p2 * per + self.j * per) * r * 4
-        side = self._side_stream if self._overlap_rs else None
-        if side is not None:  # the reduction of the piece runs beside the core GEMM (nystrom_core)
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side):
-                self._reduce(sb, off, per * r, piece)
-        else:
-            self._reduce(sb, off, per * r, piece)
+        self._reduce(sb, off, per * r, piece)
         self.comm_bytes += 4 * per * r * (p2 - 1)
         return piece[: b - a], (a, b)
 
@@ -595,34 +582,8 @@ class DistSketch:
 
     # ------------------------------------------------------------------ Alg. 2 (No-Redist)
     def nystrom_core(self, A_blk, A_tail=None):
-        """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank.
-
-        2D / column layouts with the peer-read reduce-scatter and the fused AllReduce overlap the two
-        collectives' inputs: C's partial is computed from this rank's OWN un-reduced B-bar over all rows
-        of its row block R_i (sum over all ranks of Omega_{R_i}^T B-bar_ij = sum_i Omega_{R_i}^T B_{R_i}
-        = Omega^T B), so the core GEMM runs while the reduction of the B piece (the
-        reduce-scatter) proceeds on a side stream."""
-        import torch
-        overlap = (self.world > 1 and self.fused_ar and self.layout.p2 > 1 and self.rs_mode == "peer"
-                   and self.overlap_core and torch.cuda.is_available() and A_blk.is_cuda)
-        if overlap and self._side_stream is None:
-            self._side_stream = torch.cuda.Stream(device=A_blk.device)
-        self._overlap_rs = overlap
-        self._last_bbar = None
-        try:
-            Bp, (a, b) = self.apply(A_blk, A_tail)
-        finally:
-            self._overlap_rs = False
-        if overlap and self._last_bbar is not None:
-            r0 = self.row_bnd[self.i]
-            C = self._core_fused_allreduce(self._last_bbar, r0)
-            torch.cuda.current_stream().wait_stream(self._side_stream)  # the B piece is reduced
-            if C is not None:
-                return Bp, (a, b), C
-            C = self.local.core_block(self._last_bbar, r0)
-            self.comm.all_reduce(C)
-            self.comm_bytes += C.numel() * 4
-            return Bp, (a, b), C
+        """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank."""
+        Bp, (a, b) = self.apply(A_blk, A_tail)
         if self.world > 1 and self.fused_ar:
             C = self._core_fused_allreduce(Bp, a)
             if C is not None:

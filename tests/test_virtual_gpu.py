@@ -23,7 +23,7 @@ SEED = 42
 
 
 def _run(world, spec, n1, n2, r, dist, mode, A, rs="nccl", fused_ar=False, variant="noredist", steps=2,
-         omega="accurate", overlap=False):
+         omega="accurate"):
     import paper_2603_20966_b200 as sk
     from paper_2603_20966_b200.dist import DistSketch, Layout, run_virtual
 
@@ -31,7 +31,6 @@ def _run(world, spec, n1, n2, r, dist, mode, A, rs="nccl", fused_ar=False, varia
         layout = Layout.parse(spec, world)
         local = sk.Sketch(SEED, dist, n2, r, mode=mode, omega=omega)
         ds = DistSketch(SEED, dist, n1, n2, r, layout, local=local, fused_rs=rs, fused_ar=fused_ar, comm=comm)
-        ds.overlap_core = overlap
         r0, r1, c0, c1 = ds.a_block_range()
         Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1])).cuda()
         outs = []
@@ -132,17 +131,6 @@ def test_virtual_gaussian_tf32x3_tolerance(world, spec, variant):
     # C is replicated: every rank holds the same bits
     for rk in res[1:]:
         assert np.array_equal(rk["outs"][0][3], res[0]["outs"][0][3])
-
-
-@pytest.mark.parametrize("world,spec", [(2, "col"), (4, "2x2"), (8, "4x2")])
-def test_virtual_overlapped_core_exact(world, spec):
-    """The opt-in overlap (core GEMM on the local un-reduced B-bar over the whole row block, beside the
-    reduce-scatter of the B piece on a side stream): still exactly the oracle's B and C."""
-    n, r = 1120, 48
-    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
-    Bref, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
-    res = _run(world, spec, n, n, r, "rademacher", "tf32", A, rs="peer", fused_ar=True, overlap=True, steps=3)
-    _check_exact(res, Bref, Cref, n)
 
 
 @pytest.mark.parametrize("world,spec", [(2, "col"), (4, "2x2")])
