@@ -240,13 +240,14 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     // win: clusters of 6 CTAs pack 22 per B200 (132 SMs) against 15 of 8 CTAs (120 SMs), at 4/3
     // the generated elements per A byte (c2: 2.05 -> 1.98 ms, 25000^2: 0.571 -> 0.538 ms, 12500 x
     // 50000: 0.591 -> 0.533, 6250 x 50000: 0.359 -> 0.343; the accurate transform loses, c2 2.11 ->
-    // 2.22 ms, 12500 x 50000 0.600 -> 0.631).  Only for n1 >= 4 units of 1536 rows, so the ragged
+    // 2.22 ms, 12500 x 50000 0.600 -> 0.631); tf32 with the fast transform likewise (c2: 2.369 -> 2.224
+    // ms, round 2, r2ax).  Only for n1 >= 4 units of 1536 rows, so the ragged
     // last unit stays a small share (c4, n1 = 2048, keeps one 2048-row unit).
     const bool fast = h->omega_transform == SK_OMEGA_FAST;
     if (P.ncol == 2) {
         // (chosen above)
     } else if (h->cl_override == 0 && !x3) {
-        P.cl = (bf && fast && n1 >= 4 * 1536 && cl_ok(3)) ? 3 : cl_ok(4) ? 4 : cl_ok(2) ? 2 : 1;
+        P.cl = (fast && n1 >= 4 * 1536 && cl_ok(3)) ? 3 : cl_ok(4) ? 4 : cl_ok(2) ? 2 : 1;
     } else if (h->cl_override >= 2) {
         P.cl = cl_ok(h->cl_override) ? h->cl_override : 1;
     }

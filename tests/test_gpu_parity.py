@@ -695,3 +695,17 @@ def test_three_column_passes_with_pieces(mode):
     A = synth.uniform(42, n1, n2)
     B = sk.Sketch(SEED, "gaussian", n2, r, mode=mode).apply(_dev(A)).cpu().numpy()
     assert _relF(B, oracle.sketch(SEED, "gaussian", A, r)) <= TOL[mode]
+
+
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+def test_fast_transform_clusters_of_three(mode, capfd, monkeypatch):
+    """With the fast transform, tf32 and bf16 both take clusters of 3 CTA pairs (uneven 42/43/43-row
+    shares of each Omega slice) at n1 >= 6144: against the oracle."""
+    sk = _sk()
+    monkeypatch.setenv("SK_DEBUG_PLAN", "1")
+    n1, n2, r = 6200, 2000, 256
+    A = synth.uniform(51, n1, n2)
+    B = sk.Sketch(SEED, "gaussian", n2, r, mode=mode, omega="fast").apply(_dev(A)).cpu().numpy()
+    plan = [l for l in capfd.readouterr().err.splitlines() if "sketch plan" in l]
+    assert plan and " cl=3 " in plan[-1], plan
+    assert _relF(B, oracle.sketch(SEED, "gaussian", A, r)) <= TOL[mode]
