@@ -88,12 +88,13 @@ sk_status_t sketch_set_mode(sk_sketch_t h, sk_mode_t mode);
 /* Gaussian transform used INSIDE the GEMMs (sketch_generate always uses the accurate one).
  * SK_OMEGA_FAST with SK_MODE_TF32X3 is rejected at apply time with SK_ERR_UNSUPPORTED. */
 sk_status_t sketch_set_omega_transform(sk_sketch_t h, sk_omega_transform_t t);
-/* Tuning override for the split-K factor of the sketch GEMM (0 = automatic, else 1..64). */
+/* Tuning override for the split-K factor of the sketch GEMM (0 = automatic, else 1..64).  In tf32x3
+ * the accuracy does not depend on it: TMEM accumulates at most 1024 K per chunk whatever the split. */
 sk_status_t sketch_set_split_k(sk_sketch_t h, int32_t split_k);
 
 /* Tuning / ablation override of the sketch GEMM's CTA grouping: 0 = automatic (CTA pairs with
  * tcgen05 cta_group::2 for n1 > 256; Gaussian Omega in tf32 / bf16: clusters of 4 pairs sharing the
- * generated slices for n1 >= 2048, of 3 pairs for bf16 with SK_OMEGA_FAST at n1 >= 6144; for
+ * generated slices for n1 >= 2048, of 3 pairs with SK_OMEGA_FAST at n1 >= 6144; for
  * 256 < r <= 512 (or r a multiple of 512) with Gaussian / uniform Omega in tf32 / bf16, one pass per
  * 512 columns with two N = 256 column blocks per CTA in clusters of 8 pairs = 16 CTAs, or 4 pairs
  * where 16-CTA clusters do not fit), 1 = single-CTA tiles, 2 = CTA pairs without sharing,
