@@ -411,6 +411,9 @@ def main():
                          "from the profiled eager pass that precedes them")
     ap.add_argument("--nccl-ar", action="store_true",
                     help="AllReduce C with NCCL instead of the default fused NVLink peer-read sum (f1, symmetric memory)")
+    ap.add_argument("--ar", default="sum", choices=["sum", "epilogue"],
+                    help="AllReduce of C over symmetric memory: a fixed-order sum after one barrier (default), "
+                         "or issued from the core GEMM's epilogue as in-switch multimem reductions (f1)")
     ap.add_argument("--rs", default="peer", choices=["nccl", "peer", "epilogue"],
                     help="reduce-scatter of partial B in column / 2D layouts: NCCL, symmetric-memory peer-read "
                          "sum (default), or stores from the GEMM epilogue into the owners' slots (f1)")
@@ -466,7 +469,7 @@ def main():
     if layout.p2 == 1 and world > 1 and args.balance:
         unit = local.plan_info(-(-n1 // world), n2)["rows_per_unit"]
     ds = DistSketch(SEED_OMEGA, W["dist"], n1, n2, r, layout, local=local, fused_rs=args.rs,
-                    fused_ar=not args.nccl_ar, balance_unit=unit)
+                    fused_ar=("epilogue" if args.ar == "epilogue" else not args.nccl_ar), balance_unit=unit)
     r0, r1, c0, c1 = ds.a_block_range()
     t_gen = time.perf_counter()
     A = make_A_block(W, args.workload, r0, r1, c0, c1, dev)

@@ -158,6 +158,18 @@ sk_status_t sketch_reduce_slots(sk_sketch_t h, const float* slots, int32_t nslot
  * Errors: SK_ERR_INVALID_VALUE, SK_ERR_SHAPE_MISMATCH, SK_ERR_ALIGNMENT. */
 sk_status_t sketch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, void* stream);
 
+/* The Nystrom core's AllReduce issued from the core GEMM's epilogue (PAPER.md:611 and
+ * the GPU AllReduce of C): ADDS Omega[i0 : i0+m, :r]^T B_blk into C on every rank
+ * of a multicast group -- each CTA's partial tile goes out as multimem.red.add.f32 on the multicast
+ * address C_mc (row stride ldc), reduced inside the NVSwitch; no partial workspace, no reduce kernel.
+ * The caller zeroes every rank's C and orders that (a barrier) before any rank calls this, and
+ * barriers again before reading C.  The in-switch summation order is the hardware's: C is exact in
+ * the integer regime and within fp32 rounding otherwise, but not bit-reproducible run to run.
+ * B_blk: device, 16-B aligned rows; C_mc: multicast virtual address, 16-B aligned, ldc % 4 == 0.
+ * Errors: as core_apply_block, SK_ERR_ALIGNMENT, SK_ERR_UNSUPPORTED (B rows not TMA-addressable). */
+sk_status_t core_apply_block_mc(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb, int64_t i0,
+                                float* C_mc, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
 /* NVLS reduction (the AllReduce of C, and the reduce-scatter of
  * partial B, done inside the NVSwitch): out[i] = sum over the ranks of a multicast
  * group of their copies of element i, for i < elems, read through the group's multicast mapping

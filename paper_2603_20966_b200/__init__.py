@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = (
     "sketch_create", "sketch_destroy", "sketch_set_mode", "sketch_set_omega_transform",
     "sketch_set_split_k", "sketch_set_cta_group", "sketch_set_core_impl", "sketch_set_ablation", "sketch_set_trace",
     "sketch_workspace_size", "sketch_apply", "nystrom_core",
-    "sketch_apply_block", "core_apply_block", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
+    "sketch_apply_block", "core_apply_block", "core_apply_block_mc", "core_apply_block_cols", "sketch_generate", "sketch_generate_bits",
     "sketch_rs_split", "sketch_plan_info", "sketch_apply_block_rs", "sketch_reduce_slots", "sketch_sum_peers", "sketch_multimem_sum", "sketch_pack_cols",
     "sketch_host_workspace_size", "sketch_apply_host", "nystrom_core_host",
     "sketch_debug_box_muller", "sketch_set_profiling", "sketch_profile_read", "sketch_launch_count",
@@ -88,6 +88,7 @@ def load_library(build_if_missing: bool = True):
         lib.sketch_reduce_slots.argtypes = [vp, vp, i32, i64, i64, vp, i64, vp]
         lib.sketch_sum_peers.argtypes = [ctypes.POINTER(vp), i32, i64, vp, vp]
         lib.sketch_multimem_sum.argtypes = [vp, i64, vp, vp, vp]
+        lib.core_apply_block_mc.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, ctypes.c_size_t, vp]
         lib.sketch_plan_info.argtypes = [vp, i64, i64, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
                                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         lib.sketch_pack_cols.argtypes = [vp, i64, i64, ctypes.POINTER(i64), i32, vp, vp]
@@ -306,6 +307,17 @@ class Sketch:
                                           out.data_ptr(), out.stride(0), ws.data_ptr(), ws.numel() * 4,
                                           _stream_ptr(stream)))
         return out
+
+    def core_block_mc(self, B_blk, i0: int, c_mc: int, ldc: int, stream=None):
+        """Adds Omega[i0:i0+m]^T B_blk into C on every rank of a multicast group (core_apply_block_mc)."""
+        _require_cuda(B_blk)
+        m = B_blk.shape[0]
+        ws = self.workspace(m, B_blk.device)
+        _check(self._lib.core_apply_block_mc(self._h, ctypes.c_void_p(B_blk.data_ptr()), ctypes.c_int64(m),
+                                             ctypes.c_int64(B_blk.stride(0) if m else self.r), ctypes.c_int64(i0),
+                                             ctypes.c_void_p(int(c_mc)), ctypes.c_int64(ldc),
+                                             ctypes.c_void_p(ws.data_ptr()), ctypes.c_size_t(ws.numel() * 4),
+                                             _stream_ptr(stream)))
 
     def core_block_cols(self, B_blk, i0: int, out=None, stream=None):
         """C[:, cols] = Omega[i0:i0+m]^T B_blk for a column block of B (Redist variant)."""

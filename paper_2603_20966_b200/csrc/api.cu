@@ -527,10 +527,13 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
 
 // C[r x r] (ldc) = Omega[i0 : i0+m, :r]^T * B[m x r]
 sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, int64_t i0,
-                      float* C, int64_t ldc, void* ws, cudaStream_t stream, int64_t nb = -1) {
+                      float* C, int64_t ldc, void* ws, cudaStream_t stream, int64_t nb = -1,
+                      float* C_mc = nullptr) {
     if (nb < 0) nb = h->r;
     CorePlan CP = plan_core(h, m, i0, nb);
     if (CP.tc && (!aligned16(B) || (ldb & 3))) CP = plan_core_simt(h, m);  // TMA needs 16-B rows
+    if (C_mc && !CP.tc) return fail(SK_ERR_UNSUPPORTED, "multicast core needs the tcgen05 core (16-B aligned B rows)");
+    if (C_mc && m == 0) return SK_SUCCESS;  // nothing to add
     if (CP.tc && m > 0) {
         CUtensorMap map;
         if (sk_status_t st = make_map_2d(&map, B, m, nb, ldb, 32, 32, false)) return st;
@@ -549,7 +552,9 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
         q.key1 = static_cast<uint32_t>(h->seed >> 32);
         // partials [nchunks * r, r] stored by TMA in 32x32 tiles when r is a multiple of 32
         CUtensorMap omap;
-        q.tma_store = (h->r % 32 == 0 && nb % 4 == 0 && aligned16(ws)) ? 1 : 0;
+        q.tma_store = (!C_mc && h->r % 32 == 0 && nb % 4 == 0 && aligned16(ws)) ? 1 : 0;
+        q.mc_out = C_mc;
+        q.ldc_mc = ldc;
         if (q.tma_store) {
             if (sk_status_t st = make_map_2d(&omap, q.part, static_cast<int64_t>(q.nchunks) * h->r, nb, nb, 32, 32))
                 return st;
@@ -563,6 +568,7 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
                                         h->mode == sk::kTF32x3, stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "core_gemm_tc launch");
+        if (C_mc) return SK_SUCCESS;  // the epilogue added every partial into C on every rank
         {
             LaunchScope ls(h, SK_PHASE_CORE_REDUCE, stream);
             e = sk::launch_core_reduce(q.part, q.nchunks, q.r, q.nb, C, ldc, stream);
@@ -908,6 +914,21 @@ sk_status_t core_apply_block(sk_sketch_t h, const float* B_blk, int64_t m, int64
     if (ws_bytes < need || !ws)
         return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_workspace_size");
     return core_impl(h, B_blk, m, ldb, i0, C_part, ldc, ws, static_cast<cudaStream_t>(stream));
+}
+
+sk_status_t core_apply_block_mc(sk_sketch_t h, const float* B_blk, int64_t m, int64_t ldb, int64_t i0,
+                                float* C_mc, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+    if (check_handle(h)) return SK_ERR_INVALID_VALUE;
+    if (sk_status_t st = check_mode(h)) return st;
+    if (m < 0 || i0 < 0 || i0 + m > h->n2)
+        return fail(SK_ERR_SHAPE_MISMATCH, "Omega rows [i0, i0+m) exceed the handle's n2");
+    if ((m > 0 && !B_blk) || !C_mc) return fail(SK_ERR_INVALID_VALUE, "NULL matrix pointer");
+    if (ldb < h->r || ldc < h->r) return fail(SK_ERR_SHAPE_MISMATCH, "ldb / ldc < r");
+    if (!aligned16(C_mc) || (ldc & 3)) return fail(SK_ERR_ALIGNMENT, "C_mc and ldc must be 16-byte aligned");
+    const size_t need = core_ws_bytes(h, std::max<int64_t>(m, 1));
+    if (ws_bytes < need || !ws)
+        return fail(SK_ERR_WORKSPACE, "workspace smaller than sketch_workspace_size");
+    return core_impl(h, B_blk, m, ldb, i0, nullptr, ldc, ws, static_cast<cudaStream_t>(stream), -1, C_mc);
 }
 
 sk_status_t core_apply_block_cols(sk_sketch_t h, const float* B_blk, int64_t m, int64_t nb, int64_t ldb,

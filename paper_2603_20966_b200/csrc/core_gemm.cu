@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
             for (int a = 0; a < NACC; ++a) {
                 const int row = a_off + a * 128 + q * 32 + static_cast<int>(lane);  // Omega column a
                 float* orow = out + static_cast<int64_t>(row) * p.ldp + b_off;
-                if (p.tma_store && a_off + a * 128 + q * 32 >= p.r) continue;  // padding rows of the last block
+                if ((p.tma_store || p.mc_out) && a_off + a * 128 + q * 32 >= p.r) continue;  // padding rows
 #pragma unroll 1
                 for (int cc = 0; cc < p.npad; cc += 32) {
                     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -319,7 +319,28 @@ __global__ void __launch_bounds__(kCoreThreads, 1)
                         for (int i = 0; i < 16; ++i) { v[i] = h[i]; v[16 + i] = 0u; }
                     }
                     tmem_ld_wait();
-                    if (p.tma_store) {
+                    if (p.mc_out != nullptr) {
+                        // the AllReduce issued from the epilogue: add this partial into C on every
+                        // rank of the multicast group, reduced inside the NVSwitch
+                        if (row < p.r) {
+                            float* dst = p.mc_out + static_cast<int64_t>(row) * p.ldc_mc + b_off + cc;
+                            if (b_off + cc + 32 <= p.nb) {
+#pragma unroll
+                                for (int i = 0; i < 32; i += 4)
+                                    asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + i),
+                                                 "f"(__uint_as_float(v[i])), "f"(__uint_as_float(v[i + 1])),
+                                                 "f"(__uint_as_float(v[i + 2])), "f"(__uint_as_float(v[i + 3]))
+                                                 : "memory");
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i)
+                                    if (b_off + cc + i < p.nb)
+                                        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(dst + i),
+                                                     "f"(__uint_as_float(v[i]))
+                                                     : "memory");
+                            }
+                        }
+                    } else if (p.tma_store) {
                         epi_store_tile(&tmOut, epi, ebuf, v, b_off + cc, chunk * p.r + a_off + a * 128 + q * 32);
                     } else if (row < p.r) {
 #pragma unroll

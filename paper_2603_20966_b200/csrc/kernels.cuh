@@ -85,6 +85,8 @@ struct CoreTcParams {
     int32_t nchunks;
     int32_t tma_store;    // 1: epilogue stores 32x32 tiles with TMA through tmOut (r % 32 == 0)
     uint32_t key0, key1;
+    float* mc_out;        // non-NULL: the epilogue ADDS each partial into C on every rank of a multicast
+    int64_t ldc_mc;       // group (multimem.red at mc_out + a * ldc_mc + b), instead of storing partials
 };
 
 struct LaunchCfg {

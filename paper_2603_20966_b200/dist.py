@@ -346,9 +346,14 @@ class DistSketch:
         self.fused_rs = self.rs_mode != "nccl"
         self._rs = None
         self._rsp = None
-        # f1: the AllReduce of C as one NVLink peer-read sum instead of NCCL (symmetric memory)
+        # f1: the AllReduce of C without NCCL (symmetric memory): True = every rank's core partial in its
+        # slot, one barrier, a fixed-order sum (NVLink peer reads or NVLS ld_reduce; deterministic);
+        # "epilogue" = the core GEMM's epilogue adds its partial tiles into C on every rank through the
+        # multicast mapping (multimem.red; no partial workspace, no reduce kernel; not bit-reproducible)
+        self.ar_mode = "epilogue" if fused_ar == "epilogue" else ("sum" if fused_ar else "nccl")
         self.fused_ar = bool(fused_ar) and r % 4 == 0
         self._ar = None
+        self._arm = None
         self.fallbacks = []  # (what, error) of symmetric-memory setups that fell back to NCCL
         # f1 over NVLS: symmetric-memory reductions inside the NVSwitch when the buffers have a
         # multicast mapping (SK_NVLS=0: NVLink peer reads instead)
@@ -584,6 +589,10 @@ class DistSketch:
     def nystrom_core(self, A_blk, A_tail=None):
         """Returns (B_piece, rows, C) with C = Omega^T A Omega replicated on every rank."""
         Bp, (a, b) = self.apply(A_blk, A_tail)
+        if self.world > 1 and self.fused_ar and self.ar_mode == "epilogue":
+            C = self._core_epilogue_allreduce(Bp, a)
+            if C is not None:
+                return Bp, (a, b), C
         if self.world > 1 and self.fused_ar:
             C = self._core_fused_allreduce(Bp, a)
             if C is not None:
@@ -593,6 +602,30 @@ class DistSketch:
             self.comm.all_reduce(C)
             self.comm_bytes += C.numel() * 4
         return Bp, (a, b), C
+
+    def _core_epilogue_allreduce(self, Bp, a):
+        """AllReduce of C issued from the core GEMM's epilogue: every rank zeroes its copy
+        of a symmetric r x r buffer, barrier, the core GEMM adds each partial tile into all ranks' copies
+        through the multicast mapping (multimem.red inside the NVSwitch), barrier, C = this rank's copy.
+        Returns None (and switches to the fixed-order sum) without a multicast mapping."""
+        import torch
+        r = self.r
+        if self._arm is None:
+            sb = self._symm(self.comm, (r * r,), Bp.device, "epilogue AllReduce")
+            ok = self.comm.agree(sb is not None and bool(sb.multicast_ptr), Bp.device)
+            if not ok:
+                self.ar_mode = "sum"
+                self.fallbacks.append(("epilogue AllReduce", "no multicast mapping"))
+                return None
+            self._arm = {"sb": sb}
+        sb = self._arm["sb"]
+        sb.tensor.zero_()
+        sb.barrier()  # every rank's copy is zero (and every rank has read the previous C)
+        self.local.core_block_mc(Bp, a, sb.multicast_ptr, r)
+        sb.barrier()  # every rank's reductions have landed in every copy
+        self.reduce_path = "nvls-epilogue"
+        self.comm_bytes += r * r * 4
+        return sb.tensor.view(r, r).clone()
 
     def _core_fused_allreduce(self, Bp, a):
         """AllReduce of the r x r core partials without NCCL: each rank's core GEMM

@@ -210,3 +210,58 @@ def test_all_variants_nccl_match_oracle(world):
                 assert path == ("nvls" if mc else "peer"), (path, mc)
                 if spec != "row":
                     assert rs_mode == "peer"
+
+
+def _worker_ar_epi(rank, world, port, n, r, q):
+    import torch.distributed as tdist
+    import paper_2603_20966_b200 as sk
+    from inputs import synth
+    from paper_2603_20966_b200.dist import DistSketch, Layout
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    tdist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+        local = sk.Sketch(SEED, "rademacher", n, r, mode="tf32")
+        ds = DistSketch(SEED, "rademacher", n, n, r, Layout.parse("row", world), local=local, fused_ar="epilogue")
+        r0, r1, c0, c1 = ds.a_block_range()
+        Ablk = torch.from_numpy(np.ascontiguousarray(A[r0:r1, c0:c1])).to(dev)
+        Cs = []
+        for _ in range(3):
+            Bp, (a, b), C = ds.nystrom_core(Ablk)
+            Cs.append(C.cpu().numpy())
+        torch.cuda.synchronize()
+        q.put((rank, Cs, ds.ar_mode, ds.reduce_path))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_epilogue_allreduce_multicast_matches_oracle():
+    """The AllReduce of C issued from the core GEMM's epilogue (multimem.red through the multicast
+    mapping): exact against the oracle in the integer regime on every rank, every step."""
+    import torch.multiprocessing as mp
+    import oracle
+    from inputs import synth
+    world, n, r = 2, 2100, 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ar_epi, args=(i, world, port, n, r, q)) for i in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    A = synth.int_matrix(7, n, n, -4, 4, symmetric=True)
+    _, Cref = oracle.nystrom_core(SEED, "rademacher", A, r)
+    for rank, Cs, mode, path in res:
+        if mode != "epilogue":
+            pytest.skip("no multicast mapping on this box")
+        assert path == "nvls-epilogue"
+        for C in Cs:
+            assert np.array_equal(C.astype(np.float64), Cref)
