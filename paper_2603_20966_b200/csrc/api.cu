@@ -200,6 +200,9 @@ SketchPlan plan_sketch(const sk_sketch_s* h, int64_t n1, int64_t k, int kshift, 
     };
     int a_cap = 6;
     if (bf && P.cg == 2) { a_cap = 3; P.o_stages = 8; }  // bf16 pairs: 3 x 64 KB A, rest Omega ring
+    // two column blocks (32 KB Omega stages): one more A stage for one fewer Omega stage (c4, 3 runs of
+    // each: 11.26 / 11.63 / 11.53 ms vs 11.79 / 11.80 / 12.11 ms; r2bb)
+    if (bf && P.ncol == 2) { a_cap = 4; P.o_stages = 3; }
     if (const char* e = getenv("SK_A_STAGES")) a_cap = std::max(1, std::min(8, atoi(e)));    // tuning
     if (const char* e = getenv("SK_O_STAGES")) P.o_stages = std::max(1, std::min(8, atoi(e)));  // tuning
     // bf16: the second fp32 K half of each A stage lives in a short ring of its own (freed once
