@@ -121,6 +121,24 @@ __device__ __forceinline__ void red_add_v4(float* p, uint32_t a, uint32_t b, uin
 __device__ __forceinline__ void red_add(float* p, uint32_t a) {
     asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(p), "f"(__uint_as_float(a)) : "memory");
 }
+// ... with an L2 evict-last hint: the tf32x3 output rows are added to again 1024 K later, while the
+// A stream (evict-first) passes through L2; keeping them resident avoids refetching them from DRAM
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_relaxed_v4_el(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
+    asm volatile("st.relaxed.gpu.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b),
+                 "r"(c), "r"(d), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_v4_el(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                 "f"(__uint_as_float(a)), "f"(__uint_as_float(b)), "f"(__uint_as_float(c)), "f"(__uint_as_float(d)),
+                 "l"(pol)
+                 : "memory");
+}
 
 constexpr uint32_t kATileBytes = 128 * 32 * 4;  // one 128-row x 32-fp32 TMA box
 constexpr int kMaxStages = 8;
@@ -303,6 +321,7 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
     auto drain = [&](uint32_t q, int mb, int s, bool first, uint32_t nd) {
         mbar_wait(tmem_full, nd & 1);
         tc_fence_after();
+        const uint64_t pol_el = X3 ? l2_policy_evict_last() : 0ull;
         float* out = p.out + ((!p.inplace && (p.split > 1 || p.sk_len > 0)) ? static_cast<int64_t>(s) * p.part_stride : 0);
         const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
 #pragma unroll 1
@@ -339,8 +358,10 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
                         // ordered by program order (same address), so the sum order is fixed
                         if (vec_ok && cc + 32 <= rv) {
 #pragma unroll
-                            for (int i = 0; i < 32; i += 4)
-                                red_add_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            for (int i = 0; i < 32; i += 4) {
+                                if constexpr (X3) red_add_v4_el(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3], pol_el);
+                                else red_add_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            }
                         } else {
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
@@ -350,7 +371,7 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
 #pragma unroll
                         for (int i = 0; i < 32; i += 4) {
                             if constexpr (X3)  // later chunks add to it: a strong store, ordered before them
-                                st_relaxed_v4(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                                st_relaxed_v4_el(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3], pol_el);
                             else
                                 *reinterpret_cast<float4*>(orow + cc + i) =
                                     make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
