@@ -123,11 +123,6 @@ __device__ __forceinline__ void red_add(float* p, uint32_t a) {
 }
 // ... with an L2 evict-last hint: the tf32x3 output rows are added to again 1024 K later, while the
 // A stream (evict-first) passes through L2; keeping them resident avoids refetching them from DRAM
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
 __device__ __forceinline__ void st_relaxed_v4_el(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
     asm volatile("st.relaxed.gpu.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b),
                  "r"(c), "r"(d), "l"(pol)
