@@ -123,6 +123,18 @@ __device__ __forceinline__ void red_add(float* p, uint32_t a) {
 }
 // ... with an L2 evict-last hint: the tf32x3 output rows are added to again 1024 K later, while the
 // A stream (evict-first) passes through L2; keeping them resident avoids refetching them from DRAM
+// 256-bit stores (STG.E.256): a whole 32-byte L2 sector per instruction, so a sector is never left
+// partially written -- a later reduction on a partial sector makes L2 fetch it from DRAM first
+__device__ __forceinline__ void st_v8(float* p, const uint32_t* v) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v8_el(float* p, const uint32_t* v, uint64_t pol) {
+    asm volatile("st.relaxed.gpu.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void st_relaxed_v4_el(float* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t pol) {
     asm volatile("st.relaxed.gpu.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a), "r"(b),
                  "r"(c), "r"(d), "l"(pol)
@@ -319,6 +331,8 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
         const uint64_t pol_el = X3 ? l2_policy_evict_last() : 0ull;
         float* out = p.out + ((!p.inplace && (p.split > 1 || p.sk_len > 0)) ? static_cast<int64_t>(s) * p.part_stride : 0);
         const bool vec_ok = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+        const bool vec8_ok = ((p.ldo & 7) == 0) && ((reinterpret_cast<uintptr_t>(out) & 31) == 0) &&
+                             (p.npad % 8 == 0) && p.rs_ndst == 0;
 #pragma unroll 1
         for (int ac = 0; ac < NACC * NCOL; ++ac) {
             const int a = ac / NCOL, h = ac % NCOL;
@@ -362,10 +376,18 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
                             for (int i = 0; i < 32; ++i)
                                 if (cc + i < rv) red_add(orow + cc + i, v[i]);
                         }
+                    } else if (vec8_ok && cc + 32 <= rv) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 8) {
+                            if constexpr (X3)  // later chunks add to it: a strong store, ordered before them
+                                st_relaxed_v8_el(orow + cc + i, v + i, pol_el);
+                            else
+                                st_v8(orow + cc + i, v + i);
+                        }
                     } else if (vec_ok && cc + 32 <= rv) {
 #pragma unroll
                         for (int i = 0; i < 32; i += 4) {
-                            if constexpr (X3)  // later chunks add to it: a strong store, ordered before them
+                            if constexpr (X3)
                                 st_relaxed_v4_el(orow + cc + i, v[i], v[i + 1], v[i + 2], v[i + 3], pol_el);
                             else
                                 *reinterpret_cast<float4*>(orow + cc + i) =
