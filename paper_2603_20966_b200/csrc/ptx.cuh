@@ -3,6 +3,7 @@
 // Written against the PTX ISA 8.6/8.7 forms shipped with CUDA 12.9
 // (cuda/__ptx/instructions/generated/tcgen05_*.h show the accepted spellings).
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda.h>
 
@@ -56,9 +57,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Hang detector (SK_DEBUG_HANG builds only, SURVEY §5 "race detection"): a wait that has not seen
+// its phase after ~2^SK_DEBUG_HANG_LOG2 polls prints the barrier's shared address, the parity and the
+// CTA / thread, then traps -- a missing arrival or a wrong parity becomes a launch error instead of a
+// hung GPU.  Production builds compile the plain spin.
+#ifdef SK_DEBUG_HANG
+#ifndef SK_DEBUG_HANG_LOG2
+#define SK_DEBUG_HANG_LOG2 28
+#endif
+__device__ __forceinline__ void mbar_hang_check(uint64_t& polls, uint64_t* bar, uint32_t parity) {
+    if (++polls == (1ull << SK_DEBUG_HANG_LOG2)) {
+        printf("[sketch] mbarrier wait stuck: smem 0x%x parity %u block %u thread %u\n", smem_u32(bar), parity,
+               blockIdx.x, threadIdx.x);
+        __trap();
+    }
+}
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SK_DEBUG_HANG
+    uint64_t polls = 0;
+    while (!mbar_try_wait(bar, parity)) mbar_hang_check(polls, bar, parity);
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 // Wait with a suspend-time hint (ns): the warp sleeps in the barrier unit until the phase completes
 // or the hint expires, instead of re-issuing try_wait -- for the many producer warps, so that their
@@ -75,8 +97,13 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 20000) {
+#ifdef SK_DEBUG_HANG
+    uint64_t polls = 0;
+    while (!mbar_try_wait_sleep(bar, parity, ns)) mbar_hang_check(polls, bar, parity);
+#else
     while (!mbar_try_wait_sleep(bar, parity, ns)) {
     }
+#endif
 }
 
 // ----------------------------------------------------------------------------- fences
