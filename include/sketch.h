@@ -113,7 +113,8 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt);
  * in-kernel Omega generation, bit 1 skips the A tile loads, bit 2 skips the MMAs, bit 3 runs
  * single-CTA tiles in clusters of 2, bit 4 uses release (not relaxed) cluster relays, bit 5 makes
  * the producers spin instead of suspend-waiting, bit 6 skips the converter warps' A transform
- * (bf16 conversion / tf32x3 A_lo).  0 restores normal operation. */
+ * (bf16 conversion / tf32x3 A_lo), bit 7 shrinks the cluster's Omega share copies 8x.  0 restores
+ * normal operation. */
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags);
 
 /* Pipeline trace for measurements only (libraries built with SK_BUILD_TRACE=1; otherwise a non-NULL

@@ -740,7 +740,7 @@ sk_status_t sketch_set_core_impl(sk_sketch_t h, int32_t simt) {
 
 sk_status_t sketch_set_ablation(sk_sketch_t h, uint32_t flags) {
     if (check_handle(h)) return SK_ERR_INVALID_VALUE;
-    h->ablate = flags & 127u;
+    h->ablate = flags & 255u;
     return SK_SUCCESS;
 }
 

@@ -573,7 +573,10 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
             const uint32_t half_bytes = gen_rows * 128u;  // this CTA's share of one sub-tile
             const uint32_t half_off = static_cast<uint32_t>(omega_share_row0(npad_loc, pairq)) * 128u;
             // the partners' shares land here: all rows of the slice but this CTA's own
-            const uint32_t tx = (static_cast<uint32_t>(npad_loc) - gen_rows) * 128u * (OLO ? 2u : 1u) * NSUBO;
+            uint32_t tx = (static_cast<uint32_t>(npad_loc) - gen_rows) * 128u * (OLO ? 2u : 1u) * NSUBO;
+            // ablation bit 7: copy 1/8 of each share (timing only: the result is wrong)
+            const uint32_t cp_bytes = (p.ablate & 128u) ? half_bytes / 8u : half_bytes;
+            if (p.ablate & 128u) tx /= 8u;
             uint32_t st = 0, ph = 0, ntr = 0;
             WorkIter wi(p, group);
             int mb, kb, ke, s;
@@ -592,11 +595,11 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
 #pragma unroll
                             for (int sb = 0; sb < NSUBO; ++sb) {
                                 const uint32_t src = smem_u32(sO + st * L.o_stage + L.ohi_off) + sb * osub + half_off;
-                                bulk_copy_to_cta(mapa_shared(src, partner), src, half_bytes, bar);
+                                bulk_copy_to_cta(mapa_shared(src, partner), src, cp_bytes, bar);
                             }
                             if constexpr (OLO) {
                                 const uint32_t src_lo = smem_u32(sO + st * L.o_stage + L.olo_off) + half_off;
-                                bulk_copy_to_cta(mapa_shared(src_lo, partner), src_lo, half_bytes, bar);
+                                bulk_copy_to_cta(mapa_shared(src_lo, partner), src_lo, cp_bytes, bar);
                             }
                         }
                     } else {
