@@ -36,7 +36,8 @@ for rnd in range(int(os.environ.get("ROUNDS", 3))):
     for cfg in cfgs:
         m_, o, abl = cfg[:3]
         env = cfg[3] if len(cfg) > 3 else {}
-        for k in ("SK_A_STAGES", "SK_Y_STAGES", "SK_O_STAGES", "SK_PREFETCH"): os.environ.pop(k, None)
+        for k in {"SK_A_STAGES", "SK_Y_STAGES", "SK_O_STAGES", "SK_PREFETCH"} | {k for c in cfgs if len(c) > 3 for k in c[3]}:
+            os.environ.pop(k, None)
         for k, v in env.items(): os.environ[k] = str(v)
         cg = int(env.get("CG", 0))
         for name, mod in mods:
