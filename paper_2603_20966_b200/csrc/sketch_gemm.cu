@@ -759,7 +759,11 @@ __global__ void __launch_bounds__(threads_for(MODE, NCOL, FAST), 1)
         const uint32_t hi = j8 >> 2, c0 = 2u * (j8 & 3u);
         const uint32_t ce = c0 + hi, co = c0 + 1u - hi;  // load order: even chunk first in half 0
         constexpr int kRowsPerPass = kCvtWarps * 4;        // 4 rows per warp per item
-        constexpr int kUnroll = 4;
+#ifndef SK_CVT_UNROLL
+#define SK_CVT_UNROLL 4
+#endif
+        constexpr int kUnroll = SK_CVT_UNROLL;
+        static_assert((NACC * 128) % (kRowsPerPass * kUnroll) == 0, "converter passes must tile the A stage");
         uint32_t sa = 0, pa = 0, ys = 0, ntr = 0;
         WorkIter wi(p, group);
         int mb, kb, ke, s;
