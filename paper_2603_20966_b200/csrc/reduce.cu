@@ -248,9 +248,64 @@ cudaError_t launch_accumulate(float* acc, const float* part, int64_t n, bool fir
     return cudaGetLastError();
 }
 
+// Same sums with the chunks split over 8 thread groups (many more loads in flight: the partials are
+// read from L2 right after the core GEMM wrote them).  Block = 8 groups x 32 threads over 32 float4
+// (128 consecutive elements); group g sums chunks [g C / 8, (g+1) C / 8) in increasing order, then
+// group 0 adds the 8 group sums in increasing g: a fixed bracketing of the chunk order, so reruns
+// are bit-identical.  Needs r * nb % 4 == 0 and a 16-byte aligned `part`.
+__global__ void __launch_bounds__(256) core_reduce_kernel_v4(const float* __restrict__ part, int32_t chunks,
+                                                             int32_t nb, int64_t rr, float* __restrict__ C,
+                                                             int64_t ldc) {
+    __shared__ float4 sums[8][32];
+    const int g = static_cast<int>(threadIdx.x >> 5), l = static_cast<int>(threadIdx.x & 31);
+    const int64_t i4 = static_cast<int64_t>(blockIdx.x) * 32 + l;  // float4 index
+    const bool valid = i4 * 4 < rr;
+    const int c0 = (chunks * g) / 8, c1 = (chunks * (g + 1)) / 8;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+        const float4* p4 = reinterpret_cast<const float4*>(part) + i4;
+        const int64_t cs = rr / 4;
+        int c = c0;
+        for (; c + 4 <= c1; c += 4) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = __ldcg(p4 + (c + u) * cs);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+            }
+        }
+        for (; c < c1; ++c) {
+            const float4 v = __ldcg(p4 + c * cs);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+    }
+    sums[g][l] = acc;
+    __syncthreads();
+    if (g == 0 && valid) {
+        float4 t = sums[0][l];
+#pragma unroll
+        for (int h = 1; h < 8; ++h) {
+            const float4 v = sums[h][l];
+            t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+        }
+        const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int64_t idx = i4 * 4 + e;
+            C[(idx / nb) * ldc + idx % nb] = tv[e];
+        }
+    }
+}
+
 cudaError_t launch_core_reduce(const float* part, int32_t chunks, int32_t r, int32_t nb, float* C,
                                int64_t ldc, cudaStream_t s) {
     const int64_t rr = static_cast<int64_t>(r) * nb;
+    if (rr % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15) == 0 && chunks >= 16) {
+        const int64_t blocks = (rr / 4 + 31) / 32;
+        core_reduce_kernel_v4<<<static_cast<unsigned>(blocks), 256, 0, s>>>(part, chunks, nb, rr, C, ldc);
+        return cudaGetLastError();
+    }
     const int blocks = static_cast<int>(std::min<int64_t>((rr + 255) / 256, 148 * 8));
     core_reduce_kernel<<<blocks, 256, 0, s>>>(part, chunks, r, nb, C, ldc);
     return cudaGetLastError();
