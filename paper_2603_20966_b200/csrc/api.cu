@@ -375,10 +375,25 @@ CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0, int64_t nb =
     C.nacc = (!x3 && h->r > 128) ? 2 : 1;
     C.base = i0 & ~static_cast<int64_t>(127);
     const int64_t span = std::max<int64_t>(1, i0 + m - C.base);
+    // few rows (a multi-GPU share: 6250 x 256 at 8 GPUs): even 128-row chunks leave most SMs idle, so
+    // 128-row blocks of C double the CTAs; each CTA then generates half the Omega columns (same total)
+    if (C.nacc == 2 && (span + 127) / 128 < sk::num_sms() / 2) C.nacc = 1;
     const int64_t blocks = ((h->r + 128 * C.nacc - 1) / (128 * C.nacc)) * ((nb + C.npad - 1) / C.npad);
     const int64_t want = std::max<int64_t>(1, sk::num_sms() / blocks);
     C.step = round_up((span + want - 1) / want, 128);
-    if (x3) C.step = std::min<int64_t>(C.step, 1024);
+    if (x3) {
+        // <= 1024 rows per chunk; when that leaves more CTAs than SMs (one CTA per SM), take the chunk
+        // length minimising waves x (rows + ~128 rows of fixed per-CTA cost): 50000 rows, r = 256:
+        // 1024-row chunks = 196 CTAs in 2 waves -> 768-row chunks = 264 CTAs in 2 shorter waves
+        C.step = std::min<int64_t>(C.step, 1024);
+        int64_t best = -1;
+        for (int64_t st = 128; st <= 1024; st += 128) {
+            const int64_t ctas = ((span + st - 1) / st) * blocks;
+            const int64_t cost = ((ctas + sk::num_sms() - 1) / sk::num_sms()) * (st + 128);
+            if (best < 0 || cost <= best) { best = cost; C.step = st; }
+            if (ctas <= sk::num_sms()) break;  // one wave: longer chunks only cost more
+        }
+    }
     C.chunks = static_cast<int>((span + C.step - 1) / C.step);
     return C;
 }

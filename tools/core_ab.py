@@ -13,7 +13,7 @@ for path in sys.argv[1:]:
     mods.append((path, m))
 reps = 50
 for mode in ("bf16", "tf32x3"):
-    for mrows in (6250, 12500, 50000):
+    for mrows in (int(x) for x in os.environ.get("ROWS", "6250,12500,50000").split(",")):
         B = torch.empty((mrows, 256), device='cuda').uniform_(-1, 1)
         res, outs = {}, {}
         for rnd in range(3):
