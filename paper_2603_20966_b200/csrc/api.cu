@@ -375,12 +375,33 @@ CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0, int64_t nb =
     C.nacc = (!x3 && h->r > 128) ? 2 : 1;
     C.base = i0 & ~static_cast<int64_t>(127);
     const int64_t span = std::max<int64_t>(1, i0 + m - C.base);
-    // few rows (a multi-GPU share: 6250 x 256 at 8 GPUs): even 128-row chunks leave most SMs idle, so
-    // 128-row blocks of C double the CTAs; each CTA then generates half the Omega columns (same total)
-    if (C.nacc == 2 && (span + 127) / 128 < sk::num_sms() / 2) C.nacc = 1;
+    const int64_t sms = sk::num_sms();
+    const char* core_nacc_env = getenv("SK_CORE_NACC");  // tuning: force 256 / 128-row C blocks
+    if (!x3 && h->r > 128 && h->r <= 256 && nb <= 256) {
+        // 256-row blocks of C (nacc 2) or 128-row blocks (nacc 1: twice the CTAs, each generating half
+        // the Omega columns -- the same total) and the rows per chunk: the pair minimising waves x the
+        // per-CTA time measured for r = 256 (profiles/r2_core_plan_sweep.txt: one wave takes ~19 us +
+        // 0.0625 us per row with nacc 2, ~13.5 us + 0.054 us per row with nacc 1).  6250 rows: nacc 1,
+        // 128-row chunks (27.0 -> 20.8 us); 25000: nacc 1, 384 rows (37.3 -> 35.1); 12500 / 50000 stay
+        // nacc 2 with 128 / 384 rows.
+        double best = 1e30;
+        for (int na = 2; na >= 1; --na) {
+            const int64_t blk = (h->r + 128 * na - 1) / (128 * na);
+            for (int64_t st = 128; st <= 4096; st += 128) {
+                // (depends on span only through round_up(span, 128): see core_ws_bytes)
+                const int64_t ctas = ((span + st - 1) / st) * blk;
+                const double t = static_cast<double>((ctas + sms - 1) / sms) *
+                                 (na == 2 ? 19.0 + 0.0625 * st : 13.5 + 0.054 * st);
+                if (t < best) { best = t; C.nacc = na; C.step = st; }
+                if (ctas <= sms) break;  // one wave: longer chunks only cost more
+            }
+        }
+        if (core_nacc_env) C.nacc = atoi(core_nacc_env) == 1 ? 1 : 2;  // tuning
+    }
     const int64_t blocks = ((h->r + 128 * C.nacc - 1) / (128 * C.nacc)) * ((nb + C.npad - 1) / C.npad);
-    const int64_t want = std::max<int64_t>(1, sk::num_sms() / blocks);
-    C.step = round_up((span + want - 1) / want, 128);
+    const int64_t want = std::max<int64_t>(1, sms / blocks);
+    if (x3 || !(h->r > 128 && h->r <= 256 && nb <= 256) || core_nacc_env)
+        C.step = round_up((span + want - 1) / want, 128);
     if (x3) {
         // <= 1024 rows per chunk; when that leaves more CTAs than SMs (one CTA per SM), take the chunk
         // length minimising waves x (rows + ~128 rows of fixed per-CTA cost): 50000 rows, r = 256:
@@ -394,13 +415,19 @@ CorePlan plan_core(const sk_sketch_s* h, int64_t m, int64_t i0 = 0, int64_t nb =
             if (ctas <= sk::num_sms()) break;  // one wave: longer chunks only cost more
         }
     }
+    const char* core_step_env = getenv("SK_CORE_STEP");  // tuning: rows per chunk (x 128)
+    if (core_step_env) C.step = std::max<int64_t>(128, round_up(atoi(core_step_env), 128));
     C.chunks = static_cast<int>((span + C.step - 1) / C.step);
     return C;
 }
 
 size_t core_ws_bytes(const sk_sketch_s* h, int64_t m) {
-    // chunk count of either plan for any block offset (an unaligned i0 adds at most one chunk)
-    const int64_t chunks = std::max<int64_t>(plan_core(h, m, 127).chunks + 1, plan_core_simt(h, m).chunks);
+    // largest chunk count of either plan over every block offset: i0 % 128 widens the span to m .. m + 127
+    // rows.  Chunk lengths are multiples of 128, so a tcgen05 plan's chunk count depends on the span only
+    // through round_up(span, 128) -- one of the two values the offsets 0 and 127 give (+ 1 for the
+    // round-up of the one-wave chunk length)
+    const int64_t chunks = std::max<int64_t>(
+        std::max(plan_core(h, m, 0).chunks, plan_core(h, m, 127).chunks) + 1, plan_core_simt(h, m).chunks);
     // (plan_core with nb = r: narrower column blocks -- core_apply_block_cols -- have as many chunks or fewer)
     return static_cast<size_t>(chunks) * h->r * h->r * sizeof(float);
 }
