@@ -1,5 +1,5 @@
 # CTA-grouping A/B at one shape (idle-start, interleaved): python tools/clab.py n1 n2 r mode omega cg1,cg2,...
-import os, sys, time; sys.path.insert(0, '.')
+import sys, time; sys.path.insert(0, '.')
 import torch
 import paper_2603_20966_b200 as sk
 n1, n2, r, mode, omega = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
