@@ -57,6 +57,11 @@ __device__ __forceinline__ uint4 philox_rade_call(uint64_t g, uint32_t col, uint
 // [sqrt(2)/2, sqrt(2)) by integer ops on the bit pattern; ln f = log1p(t), t = f - 1 (exact), via
 // s = t / (2 + t) and the minimax series of FreeBSD's e_logf.c (< 1 ulp); the reciprocal is the
 // approximate MUFU.RCP, whose 2^-22 error only reaches the small correction term s*(hfsq + R).
+// The Lg1..Lg4 coefficients and the k / f reduction follow FreeBSD msun's e_logf.c, which carries:
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this software is freely granted, provided
+//   that this notice is preserved.
 __device__ __forceinline__ float neg_log_u1(float u1) {
     const uint32_t ix = __float_as_uint(u1) - 0x3F3504F3u;
     const int k = static_cast<int>(ix) >> 23;                      // exponent after reduction
