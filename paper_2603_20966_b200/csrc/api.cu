@@ -577,6 +577,9 @@ sk_status_t core_impl(sk_sketch_s* h, const float* B, int64_t m, int64_t ldb, in
     if (nb < 0) nb = h->r;
     CorePlan CP = plan_core(h, m, i0, nb);
     if (CP.tc && (!aligned16(B) || (ldb & 3))) CP = plan_core_simt(h, m);  // TMA needs 16-B rows
+    // the callers validated the workspace against core_ws_bytes(h, m): the partials of this plan must fit
+    if (static_cast<size_t>(CP.chunks) * h->r * nb * sizeof(float) > core_ws_bytes(h, std::max<int64_t>(m, 1)))
+        return fail(SK_ERR_WORKSPACE, "internal: core plan exceeds the workspace bound");
     if (C_mc && !CP.tc) return fail(SK_ERR_UNSUPPORTED, "multicast core needs the tcgen05 core (16-B aligned B rows)");
     if (C_mc && m == 0) return SK_SUCCESS;  // nothing to add
     if (CP.tc && m > 0) {

@@ -709,3 +709,19 @@ def test_fast_transform_clusters_of_three(mode, capfd, monkeypatch):
     plan = [l for l in capfd.readouterr().err.splitlines() if "sketch plan" in l]
     assert plan and " cl=3 " in plan[-1], plan
     assert _relF(B, oracle.sketch(SEED, "gaussian", A, r)) <= TOL[mode]
+
+
+@pytest.mark.parametrize("mode", ["bf16", "tf32x3"])
+@pytest.mark.parametrize("m", [1, 200, 3000, 6250, 9000, 25000])
+def test_core_block_offsets_fit_queried_workspace(m, mode):
+    """The core plan is chosen per span (i0 % 128 widens it by up to 127 rows): with exactly the
+    workspace sketch_workspace_size reports for m rows, every block offset runs, and C matches the
+    oracle core (Alg. 2)."""
+    sk = _sk()
+    r = 256
+    Bm = synth.uniform(11, m, r)
+    s = sk.Sketch(SEED, "gaussian", 10**6, r, mode=mode)
+    Bd = _dev(Bm)
+    for i0 in (0, 1, 63, 64, 127, 128, 12345):
+        C = s.core_block(Bd, i0).cpu().numpy()
+        assert _relF(C, oracle.core(SEED, "gaussian", Bm.astype(np.float64), i0=i0)) <= TOL[mode], i0
