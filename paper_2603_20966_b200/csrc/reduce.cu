@@ -1,6 +1,7 @@
 // reduce.cu -- deterministic fixed-order reductions (reading R9): split-K partials of B and
 // per-chunk r x r partials of C.  Partial s is always added in increasing s.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -137,13 +138,48 @@ __global__ void sum_peers_kernel(PeerPtrs src, int32_t n, int64_t n4, float4* __
     }
 }
 
+// Compile-time rank count: all N x U loads of a thread are independent and issued before the adds
+// (NVLink reads need many requests in flight); the sum order stays rank 0, 1, ..., N-1.
+template <int N>
+__global__ void __launch_bounds__(256) sum_peers_kernel_n(PeerPtrs src, int64_t n4, float4* __restrict__ out) {
+    constexpr int kU = 2;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n4; i0 += stride * kU) {
+        float4 v[kU][N];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+                if (i0 + u * stride < n4) v[u][j] = src.p[j][i0 + u * stride];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if (i0 + u * stride >= n4) break;
+            float4 acc = v[u][0];
+#pragma unroll
+            for (int j = 1; j < N; ++j) {
+                acc.x += v[u][j].x; acc.y += v[u][j].y; acc.z += v[u][j].z; acc.w += v[u][j].w;
+            }
+            out[i0 + u * stride] = acc;
+        }
+    }
+}
+
 cudaError_t launch_sum_peers(const float* const* src, int32_t n, int64_t elems, float* out, cudaStream_t s) {
     if (n < 1 || n > 8 || (elems & 3)) return cudaErrorInvalidValue;
     PeerPtrs pp{};
     for (int j = 0; j < n; ++j) pp.p[j] = reinterpret_cast<const float4*>(src[j]);
     const int64_t n4 = elems / 4;
-    const int blocks = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 4));
-    sum_peers_kernel<<<std::max(blocks, 1), 256, 0, s>>>(pp, n, n4, reinterpret_cast<float4*>(out));
+    const int blocks = std::max(1, static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 4)));
+    float4* o = reinterpret_cast<float4*>(out);
+    if (getenv("SK_SUM_PEERS_V1") == nullptr) {  // tuning: the scalar-loop kernel
+        switch (n) {
+            case 2: sum_peers_kernel_n<2><<<blocks, 256, 0, s>>>(pp, n4, o); return cudaGetLastError();
+            case 4: sum_peers_kernel_n<4><<<blocks, 256, 0, s>>>(pp, n4, o); return cudaGetLastError();
+            case 8: sum_peers_kernel_n<8><<<blocks, 256, 0, s>>>(pp, n4, o); return cudaGetLastError();
+            default: break;
+        }
+    }
+    sum_peers_kernel<<<blocks, 256, 0, s>>>(pp, n, n4, o);
     return cudaGetLastError();
 }
 
