@@ -483,7 +483,12 @@ sk_status_t apply_impl(sk_sketch_s* h, const float* A, int64_t m, int64_t k, int
     const char* ip_env = getenv("SK_INPLACE");  // tuning: SK_INPLACE=0 keeps partials + reduce
     const char* ipm_env = getenv("SK_INPLACE_MAX");  // tuning: most pieces per m-block accumulated in place
     const int inplace_max = ipm_env ? atoi(ipm_env) : 4;
-    const bool inplace = !rs && pieces && !(ip_env && atoi(ip_env) == 0) &&
+    // Under Nsight Compute a cooperative cluster launch fails ("LaunchFailed", and ncu ends the process;
+    // r2ct): profiled runs take the partials + reduce path.  ncu exports NV_COMPUTE_PROFILER_PERFWORKS_DIR
+    // to the target (r2cv); CUDA_INJECTION64_PATH covers the other injection-based tools.
+    static const bool profiled =
+        getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr;
+    const bool inplace = !rs && pieces && !profiled && !(ip_env && atoi(ip_env) == 0) &&
                          P.split <= inplace_max && (P.sk_len > 0 || units <= ngroups || ngroups % P.split == 0);
     const size_t inplace_flag_bytes =
         static_cast<size_t>(std::max(P.num_mblk, 1)) * P.split * P.cg * P.cl * sizeof(int32_t);
